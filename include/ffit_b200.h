@@ -1,0 +1,193 @@
+/* C ABI of the B200-native likelihood engine (libffit_b200.so).
+ *
+ * Drop-in boundary for the reference engine `ffit` (arXiv 2003.12875 artifact):
+ * the `ffit_*` entry points below carry the SAME names, argument meaning, status
+ * codes and ownership rules as the reference's include/ffit.h
+ * (/root/reference/proj/include/ffit.h:1-110), so a caller that links the
+ * reference's libffit.so can relink against this library.  The computation
+ * behind ffit_nll / ffit_probabilities / ffit_fit runs on the GPU (sm_100a):
+ * datasets are SoA fp64 columns resident in HBM and the whole PDF graph plus the
+ * -log / compensated-sum reduction is one fused kernel.  There is no CPU
+ * fallback: without a usable CUDA device the evaluation calls fail with
+ * FFIT_ERR_NUMERIC and a CUDA error message.
+ *
+ * Conventions (reference include/ffit.h:1-9, src/capi.cpp:28-50): every function
+ * returns a status code; handles are opaque, caller-owned and released by the
+ * matching *_free (free(NULL) is a no-op); on failure out-parameters are left
+ * untouched and ffit_last_error() describes the failure (thread-local).
+ *
+ * The `ffcu_*` entry points are the device-level layer the north star asks for
+ * (SURVEY.md §8(b2)): multi-point launches, device-resident results for the
+ * multi-GPU exchange, zero-copy device datasets, per-PDF batch evaluation.
+ */
+#ifndef FFIT_B200_H
+#define FFIT_B200_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes -- reference include/ffit.h:20-25 */
+enum {
+  FFIT_OK = 0,
+  FFIT_ERR_USAGE = 1,
+  FFIT_ERR_DATA = 2,
+  FFIT_ERR_NUMERIC = 3,
+};
+
+/* Evaluation modes -- reference include/ffit.h:27-31, plus FFIT_MODE_GPU.
+ * BATCH_PRECISE, BATCH_FAST and GPU all run the fused sm_100a kernel;
+ * SCALAR (the reference's per-entry graph walk) is rejected with FFIT_ERR_USAGE. */
+typedef enum {
+  FFIT_MODE_SCALAR = 0,
+  FFIT_MODE_BATCH_PRECISE = 1,
+  FFIT_MODE_BATCH_FAST = 2,
+  FFIT_MODE_GPU = 3,
+} ffit_mode;
+
+typedef struct ffit_model ffit_model;
+typedef struct ffit_dataset ffit_dataset;
+typedef struct ffit_fit_result ffit_fit_result;
+
+/* reference include/ffit.h:37 */
+const char* ffit_last_error(void);
+
+/* ---- models: reference include/ffit.h:39-53 --------------------------------
+ * Model-file grammar of the reference (proj/docs/model-file.md) plus, on the
+ * GPU path: ArgusBG(x, m0, c, p), Chebychev(x, a1..an), Polynomial(x, a1..an),
+ * ProdPdf(p1, ..., pk) over distinct observables, AddPdf(c1, f1, ..., cn) (=
+ * WeightedSum) and AddPdf(c1, y1, ..., cn, yn) (extended), several
+ * `observable` lines.  Expression pdfs are rejected (no GPU kernel). */
+int ffit_model_load(const char* path, ffit_model** out);
+int ffit_model_parse(const char* text, ffit_model** out);
+void ffit_model_free(ffit_model* m);
+const char* ffit_model_observable(const ffit_model* m); /* the first observable */
+int ffit_model_observable_range(const ffit_model* m, double* lo, double* hi);
+int ffit_model_param_count(const ffit_model* m);
+const char* ffit_model_param_name(const ffit_model* m, int i);
+int ffit_model_param_is_constant(const ffit_model* m, const char* name, int* constant);
+int ffit_model_get_param(const ffit_model* m, const char* name, double* value,
+                         double* uncertainty);
+int ffit_model_set_param(ffit_model* m, const char* name, double value);
+
+/* ---- datasets: reference include/ffit.h:55-66 ------------------------------
+ * Datasets live in HBM on the CUDA device current at creation time. */
+int ffit_dataset_read_csv(const ffit_model* m, const char* path, ffit_dataset** out,
+                          long* dropped);
+int ffit_dataset_write_csv(const ffit_dataset* ds, const char* path);
+long ffit_dataset_rows(const ffit_dataset* ds);
+void ffit_dataset_free(ffit_dataset* ds);
+
+/* ---- sampling: reference include/ffit.h:68-73 ------------------------------ */
+int ffit_sample(ffit_model* m, long n, unsigned long long seed, ffit_dataset** out,
+                double* efficiency);
+
+/* ---- evaluation: reference include/ffit.h:75-85 ----------------------------
+ * *n_evaluations = kernels launched (independent of the number of events, as
+ * the reference's batch-mode call accounting). */
+int ffit_nll(ffit_model* m, const ffit_dataset* ds, ffit_mode mode, double* value,
+             unsigned long long* n_evaluations);
+int ffit_probabilities(ffit_model* m, const ffit_dataset* ds, ffit_mode mode, double* out);
+
+/* ---- fitting: reference include/ffit.h:87-104 ------------------------------
+ * The reference's Nelder-Mead (proj/src/fit.cpp:86-251) with batched GPU points. */
+int ffit_fit(ffit_model* m, const ffit_dataset* ds, ffit_mode mode, double tolerance,
+             long max_iterations, ffit_fit_result** out);
+int ffit_result_converged(const ffit_fit_result* r);
+double ffit_result_nll(const ffit_fit_result* r);
+unsigned long long ffit_result_nll_calls(const ffit_fit_result* r);
+double ffit_result_wall_seconds(const ffit_fit_result* r);
+int ffit_result_uncertainties_valid(const ffit_fit_result* r);
+int ffit_result_param_count(const ffit_fit_result* r);
+const char* ffit_result_param_name(const ffit_fit_result* r, int i);
+double ffit_result_param_value(const ffit_fit_result* r, int i);
+double ffit_result_param_uncertainty(const ffit_fit_result* r, int i);
+void ffit_result_free(ffit_fit_result* r);
+
+/* ======================= device-level layer (ffcu_*) ======================= */
+
+/* Dataset from host columns (uploaded once to HBM; replaces the reference's
+ * DataSet(names, columns) constructor, proj/include/ffit/dataset.hpp:25). */
+int ffcu_dataset_from_host(const char* const* names, const double* const* cols, int ncols,
+                           long long n, ffit_dataset** out);
+/* Zero-copy view over caller-owned device columns (e.g. torch tensors) on
+ * `device`; the memory must outlive the view. */
+int ffcu_dataset_from_device(const char* const* names, const double* const* dev_cols, int ncols,
+                             long long n, int device, ffit_dataset** out);
+/* Refill an owned dataset from host columns of the same shape. */
+int ffcu_dataset_copy_from_host(ffit_dataset* ds, const double* const* cols);
+/* Rows [begin, end) as a zero-copy view (event sharding). */
+int ffcu_dataset_slice(const ffit_dataset* ds, long long begin, long long end, ffit_dataset** out);
+int ffcu_dataset_ncols(const ffit_dataset* ds);
+const char* ffcu_dataset_column_name(const ffit_dataset* ds, int i);
+int ffcu_dataset_download(const ffit_dataset* ds, int col, double* host_out);
+int ffcu_dataset_device_column(const ffit_dataset* ds, int col, const double** dev_ptr);
+
+/* NLL at P parameter points in ONE launch.  points: P x ffit_model_param_count
+ * doubles, row-major, parameters in ffit_model_param_name order.  values[p]
+ * = NLL (+inf if an event has p <= 0 or non-finite; first_invalid[p] = its
+ * index, else -1).  first_invalid and n_evaluations may be NULL. */
+int ffcu_nll_points(ffit_model* m, const ffit_dataset* ds, const double* points, int P,
+                    double* values, long long* first_invalid, unsigned long long* n_evaluations);
+/* Same, returning the uncombined Neumaier pairs (sc[2p], sc[2p+1]) of the event
+ * sum only (no extended term) -- the per-rank partials of the multi-GPU path. */
+int ffcu_nll_points_partial(ffit_model* m, const ffit_dataset* ds, const double* points, int P,
+                            double* sc, long long* first_invalid,
+                            unsigned long long* n_evaluations);
+/* Asynchronous on `stream` (cudaStream_t; NULL = the model's stream): writes P
+ * pairs to device d_sc (2P doubles) and P indices to device d_bad
+ * (0xFFFFFFFFFFFFFFFF = none).  P <= 512. */
+int ffcu_nll_points_device(ffit_model* m, const ffit_dataset* ds, const double* points, int P,
+                           double* d_sc, unsigned long long* d_bad, void* stream,
+                           unsigned long long* n_evaluations);
+/* Fixed-rank-order compensated combine of R x P device pairs into P pairs. */
+int ffcu_combine_pairs_device(const double* d_in, int R, int P, double* d_out, void* stream);
+/* Extended term nu - N log nu per point (0 for non-extended models). */
+int ffcu_extended_terms(const ffit_model* m, const double* points, int P, double n_events,
+                        double* out);
+/* probabilities() at an explicit point (NULL = current parameter values). */
+int ffcu_probabilities_at(ffit_model* m, const ffit_dataset* ds, const double* point,
+                          double* out);
+/* PdfSpec::eval_batch (proj/include/ffit/pdfs.hpp:59-60): unnormalised values of
+ * the named (sub-)pdf over the dataset at the current parameter values. */
+int ffcu_eval_batch(ffit_model* m, const char* pdf, const ffit_dataset* ds, double* out);
+int ffcu_eval_batch_device(ffit_model* m, const char* pdf, const ffit_dataset* ds, double* d_out,
+                           void* stream);
+/* normalization(spec, lo, hi, graph) (proj/include/ffit/eval.hpp:26) of a named
+ * pdf at a point (NULL = current values). */
+int ffcu_normalization(const ffit_model* m, const char* pdf, const double* point, double* out);
+/* The flattened plan and one point's constant row (host logic, no GPU needed). */
+int ffcu_plan_info(const ffit_model* m, int* nterms, int* ncols, int* stride);
+int ffcu_plan_term(const ffit_model* m, int i, int* kind, int* col, int* order, int* flags,
+                   int* coff);
+int ffcu_point_constants(const ffit_model* m, const double* point, double* row);
+int ffcu_model_pdf_count(const ffit_model* m);
+const char* ffcu_model_pdf_name(const ffit_model* m, int i);
+int ffcu_model_observable_count(const ffit_model* m);
+const char* ffcu_model_observable_name(const ffit_model* m, int i);
+
+/* Minuit-style batched fit: BFGS on central finite differences, 2d+1 points per
+ * launch per iteration; Hessian uncertainties from one launch. */
+int ffcu_fit_gradient(ffit_model* m, const ffit_dataset* ds, double tolerance,
+                      long max_iterations, ffit_fit_result** out);
+int ffcu_result_iterations(const ffit_fit_result* r);
+unsigned long long ffcu_result_launches(const ffit_fit_result* r);
+int ffcu_result_trace(const ffit_fit_result* r, double* out, int cap);
+
+/* Last fused-NLL launch shape: threads, events/thread, tile, tiles, chunks, grid. */
+int ffcu_last_launch(const ffit_model* m, int* info6);
+/* Kernels this library has launched in this process. */
+unsigned long long ffcu_kernel_launches(void);
+/* Measured FP64 FMA instructions per second on the current device. */
+int ffcu_fp64_peak(double* fma_per_s, float* ms);
+/* Seeded generator into host columns (one per observable, each n doubles). */
+int ffcu_sample_host(ffit_model* m, long long n, unsigned long long seed, double* const* cols,
+                     double* efficiency);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FFIT_B200_H */

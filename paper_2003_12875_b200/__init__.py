@@ -1,0 +1,11 @@
+"""B200-native batched PDF-graph evaluation + unbinned NLL (arXiv 2003.12875 hot path).
+
+The product is the C-ABI library ``lib/libffit_b200.so`` (CUDA sm_100a kernels +
+C++ host engine, sources in ``csrc/``, header ``include/ffit_b200.h``); this
+package is its Python mirror of the reference interface.
+"""
+from ._lib import LIB_PATH, build, lib  # noqa: F401
+from .ffit import (  # noqa: F401
+    DataSet, EvalMode, FfitError, FitResult, Model, NllValue, eval_batch, fit_gradient, fit_to,
+    fp64_peak, kernel_launches, last_launch, nll, nll_c, nll_points, nll_points_device,
+    nll_points_partial, normalization, probabilities, sample_host)

@@ -1,0 +1,703 @@
+// extern "C" boundary (include/ffit_b200.h).  Same status-code / ownership /
+// thread-local-error contract as the reference (proj/src/capi.cpp:28-50).
+#include "../../include/ffit_b200.h"
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <limits>
+#include <memory>
+#include <sstream>
+#include <string>
+
+#include "engine.hpp"
+#include "fit.hpp"
+#include "sampler.hpp"
+
+#define FFB_API extern "C" __attribute__((visibility("default")))
+
+struct ffit_model {
+  std::unique_ptr<ffb::Model> m;
+  std::unique_ptr<ffb::Engine> engine;
+};
+
+struct ffit_dataset {
+  std::shared_ptr<ffb::DeviceDataset> d;
+};
+
+struct ffit_fit_result {
+  ffb::FitResult r;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return FFIT_OK;
+  } catch (const ffb::Error& e) {
+    g_last_error = e.what();
+    return static_cast<int>(e.code());
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return FFIT_ERR_NUMERIC;
+  }
+}
+
+void require(const void* p, const char* what) {
+  if (!p) ffb::usage_error(std::string(what) + " must not be null");
+}
+
+void require_gpu_mode(ffit_mode mode) {
+  switch (mode) {
+    case FFIT_MODE_BATCH_PRECISE:
+    case FFIT_MODE_BATCH_FAST:
+    case FFIT_MODE_GPU:
+      return;
+    case FFIT_MODE_SCALAR:
+      ffb::usage_error("scalar (per-entry graph walk) mode is the CPU reference's; this library "
+                       "evaluates on the GPU (use FFIT_MODE_GPU)");
+  }
+  ffb::usage_error("unknown evaluation mode");
+}
+
+ffb::Engine& engine(ffit_model* m) {
+  if (!m->engine) m->engine = std::make_unique<ffb::Engine>(*m->m);
+  return *m->engine;
+}
+
+std::vector<double> point_or_current(const ffb::Model& m, const double* point) {
+  if (point) return std::vector<double>(point, point + m.params.size());
+  return m.theta();
+}
+
+std::unique_ptr<ffit_model> make_model(std::unique_ptr<ffb::Model> mm) {
+  auto m = std::make_unique<ffit_model>();
+  m->m = std::move(mm);
+  m->engine = std::make_unique<ffb::Engine>(*m->m);  // compiles the plan: fail early
+  return m;
+}
+
+std::vector<std::string> split_csv(const std::string& line) {
+  std::vector<std::string> out;
+  std::string cur;
+  for (const char ch : line) {
+    if (ch == ',') {
+      out.push_back(cur);
+      cur.clear();
+    } else if (ch != '\r') {
+      cur += ch;
+    }
+  }
+  out.push_back(cur);
+  for (auto& s : out) {
+    const auto b = s.find_first_not_of(" \t");
+    const auto e = s.find_last_not_of(" \t");
+    s = b == std::string::npos ? std::string() : s.substr(b, e - b + 1);
+  }
+  return out;
+}
+
+}  // namespace
+
+FFB_API const char* ffit_last_error(void) { return g_last_error.c_str(); }
+
+// ---------------------------------------------------------------------------
+// models
+
+FFB_API int ffit_model_load(const char* path, ffit_model** out) {
+  return guarded([&] {
+    require(path, "path");
+    require(out, "out");
+    std::ifstream in(path);
+    if (!in) ffb::data_error(std::string("cannot open model file: ") + path);
+    std::ostringstream buf;
+    buf << in.rdbuf();
+    *out = make_model(ffb::Model::parse(buf.str(), path)).release();
+  });
+}
+
+FFB_API int ffit_model_parse(const char* text, ffit_model** out) {
+  return guarded([&] {
+    require(text, "text");
+    require(out, "out");
+    *out = make_model(ffb::Model::parse(text)).release();
+  });
+}
+
+FFB_API void ffit_model_free(ffit_model* m) { delete m; }
+
+FFB_API const char* ffit_model_observable(const ffit_model* m) {
+  return m->m->observables[0].name.c_str();
+}
+
+FFB_API int ffit_model_observable_range(const ffit_model* m, double* lo, double* hi) {
+  return guarded([&] {
+    require(m, "model");
+    if (lo) *lo = m->m->observables[0].lo;
+    if (hi) *hi = m->m->observables[0].hi;
+  });
+}
+
+FFB_API int ffit_model_param_count(const ffit_model* m) {
+  return static_cast<int>(m->m->params.size());
+}
+
+FFB_API const char* ffit_model_param_name(const ffit_model* m, int i) {
+  if (i < 0 || i >= static_cast<int>(m->m->params.size())) return nullptr;
+  return m->m->params[i].name.c_str();
+}
+
+FFB_API int ffit_model_param_is_constant(const ffit_model* m, const char* name, int* constant) {
+  return guarded([&] {
+    require(m, "model");
+    require(constant, "constant");
+    const int id = name ? m->m->param_index(name) : -1;
+    if (id < 0) ffb::usage_error("unknown parameter: " + std::string(name ? name : "(null)"));
+    *constant = m->m->params[id].constant ? 1 : 0;
+  });
+}
+
+FFB_API int ffit_model_get_param(const ffit_model* m, const char* name, double* value,
+                                 double* uncertainty) {
+  return guarded([&] {
+    require(m, "model");
+    const int id = name ? m->m->param_index(name) : -1;
+    if (id < 0) ffb::usage_error("unknown parameter: " + std::string(name ? name : "(null)"));
+    if (value) *value = m->m->params[id].value;
+    if (uncertainty) *uncertainty = m->m->params[id].error;
+  });
+}
+
+FFB_API int ffit_model_set_param(ffit_model* m, const char* name, double value) {
+  return guarded([&] {
+    require(m, "model");
+    const int id = name ? m->m->param_index(name) : -1;
+    if (id < 0) ffb::usage_error("unknown parameter: " + std::string(name ? name : "(null)"));
+    m->m->set_value(id, value);
+  });
+}
+
+// ---------------------------------------------------------------------------
+// datasets
+
+// DataSet::from_csv (proj/src/dataset.cpp:61-121): header line, rows outside an
+// observable's range dropped and counted; then one upload to HBM.
+FFB_API int ffit_dataset_read_csv(const ffit_model* m, const char* path, ffit_dataset** out,
+                                  long* dropped) {
+  return guarded([&] {
+    require(m, "model");
+    require(path, "path");
+    require(out, "out");
+    std::ifstream in(path);
+    if (!in) ffb::data_error(std::string("cannot open file: ") + path);
+    std::string line;
+    if (!std::getline(in, line)) ffb::data_error(std::string("empty file: ") + path);
+    const std::vector<std::string> header = split_csv(line);
+    const auto& obs = m->m->observables;
+    std::vector<std::size_t> idx(obs.size());
+    for (std::size_t s = 0; s < obs.size(); ++s) {
+      bool found = false;
+      for (std::size_t h = 0; h < header.size(); ++h) {
+        if (header[h] == obs[s].name) {
+          idx[s] = h;
+          found = true;
+          break;
+        }
+      }
+      if (!found) ffb::data_error("missing column '" + obs[s].name + "' in " + path);
+    }
+    std::vector<std::vector<double>> cols(obs.size());
+    std::vector<double> parsed(obs.size());
+    long nd = 0;
+    std::size_t row = 0;
+    while (std::getline(in, line)) {
+      ++row;
+      if (line.empty() || line == "\r") continue;
+      const std::vector<std::string> f = split_csv(line);
+      if (f.size() < header.size()) {
+        ffb::data_error("row " + std::to_string(row) + " has " + std::to_string(f.size()) +
+                        " fields, header has " + std::to_string(header.size()));
+      }
+      bool in_range = true;
+      for (std::size_t s = 0; s < obs.size(); ++s) {
+        const std::string& cell = f[idx[s]];
+        char* end = nullptr;
+        const double v = std::strtod(cell.c_str(), &end);
+        if (cell.empty() || end != cell.c_str() + cell.size()) {
+          ffb::data_error("bad number at row " + std::to_string(row) + ", column '" + obs[s].name +
+                          "': '" + cell + "'");
+        }
+        parsed[s] = v;
+        if (!(v >= obs[s].lo && v <= obs[s].hi)) in_range = false;
+      }
+      if (!in_range) {
+        ++nd;
+        continue;
+      }
+      for (std::size_t s = 0; s < obs.size(); ++s) cols[s].push_back(parsed[s]);
+    }
+    std::vector<std::string> names;
+    std::vector<const double*> ptrs;
+    for (std::size_t s = 0; s < obs.size(); ++s) {
+      names.push_back(obs[s].name);
+      ptrs.push_back(cols[s].data());
+    }
+    auto d = ffb::DeviceDataset::upload(names, ptrs, static_cast<long long>(cols[0].size()));
+    if (dropped) *dropped = nd;
+    *out = new ffit_dataset{std::move(d)};
+  });
+}
+
+// DataSet::write_csv (proj/src/dataset.cpp:123-146): %.17g round-trip.
+FFB_API int ffit_dataset_write_csv(const ffit_dataset* ds, const char* path) {
+  return guarded([&] {
+    require(ds, "dataset");
+    require(path, "path");
+    const auto& d = *ds->d;
+    std::vector<std::vector<double>> cols(d.cols.size(), std::vector<double>(static_cast<std::size_t>(d.n)));
+    for (std::size_t c = 0; c < cols.size(); ++c) d.download(static_cast<int>(c), cols[c].data());
+    std::FILE* f = std::fopen(path, "w");
+    if (!f) ffb::data_error(std::string("cannot write file: ") + path);
+    for (std::size_t c = 0; c < d.names.size(); ++c) std::fprintf(f, c ? ",%s" : "%s", d.names[c].c_str());
+    std::fputc('\n', f);
+    for (long long i = 0; i < d.n; ++i) {
+      for (std::size_t c = 0; c < cols.size(); ++c) std::fprintf(f, c ? ",%.17g" : "%.17g", cols[c][i]);
+      std::fputc('\n', f);
+    }
+    if (std::fclose(f) != 0) ffb::data_error(std::string("write failed: ") + path);
+  });
+}
+
+FFB_API long ffit_dataset_rows(const ffit_dataset* ds) { return static_cast<long>(ds->d->n); }
+
+FFB_API void ffit_dataset_free(ffit_dataset* ds) { delete ds; }
+
+FFB_API int ffit_sample(ffit_model* m, long n, unsigned long long seed, ffit_dataset** out,
+                        double* efficiency) {
+  return guarded([&] {
+    require(m, "model");
+    require(out, "out");
+    if (n < 0) ffb::usage_error("sample size must be >= 0");
+    ffb::SampleStats st;
+    const auto cols = ffb::sample(*m->m, n, seed, &st);
+    std::vector<std::string> names;
+    std::vector<const double*> ptrs;
+    for (std::size_t s = 0; s < cols.size(); ++s) {
+      names.push_back(m->m->observables[s].name);
+      ptrs.push_back(cols[s].data());
+    }
+    auto d = ffb::DeviceDataset::upload(names, ptrs, n);
+    if (efficiency) {
+      *efficiency = st.proposed == 0 ? -1.0
+                                     : static_cast<double>(st.accepted) / static_cast<double>(st.proposed);
+    }
+    *out = new ffit_dataset{std::move(d)};
+  });
+}
+
+FFB_API int ffcu_sample_host(ffit_model* m, long long n, unsigned long long seed, double* const* cols,
+                             double* efficiency) {
+  return guarded([&] {
+    require(m, "model");
+    require(cols, "cols");
+    ffb::SampleStats st;
+    const auto out = ffb::sample(*m->m, n, seed, &st);
+    for (std::size_t s = 0; s < out.size(); ++s) {
+      require(cols[s], "cols[i]");
+      std::memcpy(cols[s], out[s].data(), static_cast<std::size_t>(n) * sizeof(double));
+    }
+    if (efficiency) {
+      *efficiency = st.proposed == 0 ? -1.0
+                                     : static_cast<double>(st.accepted) / static_cast<double>(st.proposed);
+    }
+  });
+}
+
+// ---------------------------------------------------------------------------
+// evaluation
+
+FFB_API int ffit_nll(ffit_model* m, const ffit_dataset* ds, ffit_mode mode, double* value,
+                     unsigned long long* n_evaluations) {
+  return guarded([&] {
+    require(m, "model");
+    require(ds, "dataset");
+    require_gpu_mode(mode);
+    const std::vector<double> th = m->m->theta();
+    m->m->check_params(m->m->root, th.data());  // require_valid_params, proj/src/eval.cpp:120
+    const ffb::NllResult r = engine(m).nll_points(*ds->d, th.data(), 1);
+    if (value) *value = r.value[0];
+    if (n_evaluations) *n_evaluations = r.launches;
+  });
+}
+
+FFB_API int ffit_probabilities(ffit_model* m, const ffit_dataset* ds, ffit_mode mode, double* out) {
+  return guarded([&] {
+    require(m, "model");
+    require(ds, "dataset");
+    require(out, "out");
+    require_gpu_mode(mode);
+    const std::vector<double> th = m->m->theta();
+    engine(m).probabilities(*ds->d, th.data(), out, false);
+  });
+}
+
+FFB_API int ffcu_probabilities_at(ffit_model* m, const ffit_dataset* ds, const double* point,
+                                  double* out) {
+  return guarded([&] {
+    require(m, "model");
+    require(ds, "dataset");
+    require(out, "out");
+    const std::vector<double> th = point_or_current(*m->m, point);
+    engine(m).probabilities(*ds->d, th.data(), out, false);
+  });
+}
+
+FFB_API int ffcu_nll_points(ffit_model* m, const ffit_dataset* ds, const double* points, int P,
+                            double* values, long long* first_invalid,
+                            unsigned long long* n_evaluations) {
+  return guarded([&] {
+    require(m, "model");
+    require(ds, "dataset");
+    require(points, "points");
+    require(values, "values");
+    if (P < 0) ffb::usage_error("P must be >= 0");
+    if (P == 0) {
+      if (n_evaluations) *n_evaluations = 0;
+      return;
+    }
+    const ffb::NllResult r = engine(m).nll_points(*ds->d, points, P);
+    for (int p = 0; p < P; ++p) {
+      values[p] = r.value[p];
+      if (first_invalid) first_invalid[p] = r.first_invalid[p];
+    }
+    if (n_evaluations) *n_evaluations = r.launches;
+  });
+}
+
+FFB_API int ffcu_nll_points_partial(ffit_model* m, const ffit_dataset* ds, const double* points, int P,
+                                    double* sc, long long* first_invalid,
+                                    unsigned long long* n_evaluations) {
+  return guarded([&] {
+    require(m, "model");
+    require(ds, "dataset");
+    require(points, "points");
+    require(sc, "sc");
+    if (P < 0) ffb::usage_error("P must be >= 0");
+    if (P == 0) return;
+    const ffb::NllResult r = engine(m).nll_points(*ds->d, points, P);
+    for (int p = 0; p < P; ++p) {
+      sc[2 * p] = r.pairs[p].s;
+      sc[2 * p + 1] = r.pairs[p].c;
+      if (first_invalid) first_invalid[p] = r.first_invalid[p];
+    }
+    if (n_evaluations) *n_evaluations = r.launches;
+  });
+}
+
+FFB_API int ffcu_nll_points_device(ffit_model* m, const ffit_dataset* ds, const double* points, int P,
+                                   double* d_sc, unsigned long long* d_bad, void* stream,
+                                   unsigned long long* n_evaluations) {
+  return guarded([&] {
+    require(m, "model");
+    require(ds, "dataset");
+    require(points, "points");
+    require(d_sc, "d_sc");
+    require(d_bad, "d_bad");
+    const int k = engine(m).nll_points_device(*ds->d, points, P, reinterpret_cast<ffb::SumPair*>(d_sc),
+                                              d_bad, static_cast<cudaStream_t>(stream));
+    if (n_evaluations) *n_evaluations = static_cast<unsigned long long>(k);
+  });
+}
+
+FFB_API int ffcu_combine_pairs_device(const double* d_in, int R, int P, double* d_out, void* stream) {
+  return guarded([&] {
+    require(d_in, "d_in");
+    require(d_out, "d_out");
+    ffb::count_launches(ffb::launch_combine_ranks(reinterpret_cast<const ffb::SumPair*>(d_in), R, P,
+                                                  reinterpret_cast<ffb::SumPair*>(d_out),
+                                                  static_cast<cudaStream_t>(stream)));
+    ffb::cuda_check(cudaGetLastError(), "combine_ranks");
+  });
+}
+
+FFB_API int ffcu_extended_terms(const ffit_model* m, const double* points, int P, double n_events,
+                                double* out) {
+  return guarded([&] {
+    require(m, "model");
+    require(points, "points");
+    require(out, "out");
+    const std::size_t npar = m->m->params.size();
+    for (int p = 0; p < P; ++p) out[p] = m->m->extended_term(points + p * npar, n_events);
+  });
+}
+
+FFB_API int ffcu_eval_batch(ffit_model* m, const char* pdf, const ffit_dataset* ds, double* out) {
+  return guarded([&] {
+    require(m, "model");
+    require(ds, "dataset");
+    require(out, "out");
+    const int id = pdf ? m->m->pdf_index(pdf) : m->m->root;
+    if (id < 0) ffb::usage_error(std::string("unknown pdf: ") + pdf);
+    const std::vector<double> th = m->m->theta();
+    engine(m).eval_batch(id, *ds->d, th.data(), out, false);
+  });
+}
+
+FFB_API int ffcu_eval_batch_device(ffit_model* m, const char* pdf, const ffit_dataset* ds,
+                                   double* d_out, void* stream) {
+  return guarded([&] {
+    require(m, "model");
+    require(ds, "dataset");
+    require(d_out, "d_out");
+    const int id = pdf ? m->m->pdf_index(pdf) : m->m->root;
+    if (id < 0) ffb::usage_error(std::string("unknown pdf: ") + pdf);
+    const std::vector<double> th = m->m->theta();
+    engine(m).eval_batch(id, *ds->d, th.data(), d_out, true, static_cast<cudaStream_t>(stream));
+  });
+}
+
+FFB_API int ffcu_normalization(const ffit_model* m, const char* pdf, const double* point, double* out) {
+  return guarded([&] {
+    require(m, "model");
+    require(out, "out");
+    const int id = pdf ? m->m->pdf_index(pdf) : m->m->root;
+    if (id < 0) ffb::usage_error(std::string("unknown pdf: ") + pdf);
+    const std::vector<double> th = point_or_current(*m->m, point);
+    m->m->check_params(id, th.data());
+    *out = m->m->normalization(id, th.data());
+  });
+}
+
+FFB_API int ffcu_plan_info(const ffit_model* m, int* nterms, int* ncols, int* stride) {
+  return guarded([&] {
+    require(m, "model");
+    const ffb::DevPlan& p = m->engine->likelihood_plan().dev;
+    if (nterms) *nterms = p.nterms;
+    if (ncols) *ncols = p.ncols;
+    if (stride) *stride = p.stride;
+  });
+}
+
+FFB_API int ffcu_plan_term(const ffit_model* m, int i, int* kind, int* col, int* order, int* flags,
+                           int* coff) {
+  return guarded([&] {
+    require(m, "model");
+    const ffb::DevPlan& p = m->engine->likelihood_plan().dev;
+    if (i < 0 || i >= p.nterms) ffb::usage_error("term index out of range");
+    if (kind) *kind = p.t[i].kind;
+    if (col) *col = p.t[i].col;
+    if (order) *order = p.t[i].order;
+    if (flags) *flags = p.t[i].flags;
+    if (coff) *coff = p.t[i].coff;
+  });
+}
+
+FFB_API int ffcu_point_constants(const ffit_model* m, const double* point, double* row) {
+  return guarded([&] {
+    require(m, "model");
+    require(row, "row");
+    const std::vector<double> th = point_or_current(*m->m, point);
+    ffb::build_constants(m->engine->likelihood_plan(), *m->m, th.data(), row);
+  });
+}
+
+FFB_API int ffcu_model_pdf_count(const ffit_model* m) { return static_cast<int>(m->m->pdfs.size()); }
+
+FFB_API const char* ffcu_model_pdf_name(const ffit_model* m, int i) {
+  if (i < 0 || i >= static_cast<int>(m->m->pdfs.size())) return nullptr;
+  return m->m->pdfs[i].name.c_str();
+}
+
+FFB_API int ffcu_model_observable_count(const ffit_model* m) {
+  return static_cast<int>(m->m->observables.size());
+}
+
+FFB_API const char* ffcu_model_observable_name(const ffit_model* m, int i) {
+  if (i < 0 || i >= static_cast<int>(m->m->observables.size())) return nullptr;
+  return m->m->observables[i].name.c_str();
+}
+
+// ---------------------------------------------------------------------------
+// device datasets
+
+FFB_API int ffcu_dataset_from_host(const char* const* names, const double* const* cols, int ncols,
+                                   long long n, ffit_dataset** out) {
+  return guarded([&] {
+    require(names, "names");
+    require(out, "out");
+    if (ncols <= 0) ffb::usage_error("a dataset needs at least one column");
+    if (n > 0) require(cols, "cols");
+    std::vector<std::string> nm;
+    std::vector<const double*> c;
+    for (int i = 0; i < ncols; ++i) {
+      require(names[i], "names[i]");
+      nm.push_back(names[i]);
+      c.push_back(n > 0 ? cols[i] : nullptr);
+    }
+    *out = new ffit_dataset{ffb::DeviceDataset::upload(nm, c, n)};
+  });
+}
+
+FFB_API int ffcu_dataset_from_device(const char* const* names, const double* const* dev_cols, int ncols,
+                                     long long n, int device, ffit_dataset** out) {
+  return guarded([&] {
+    require(names, "names");
+    require(dev_cols, "dev_cols");
+    require(out, "out");
+    if (ncols <= 0) ffb::usage_error("a dataset needs at least one column");
+    std::vector<std::string> nm;
+    std::vector<const double*> c;
+    for (int i = 0; i < ncols; ++i) {
+      require(names[i], "names[i]");
+      nm.push_back(names[i]);
+      c.push_back(dev_cols[i]);
+    }
+    *out = new ffit_dataset{ffb::DeviceDataset::view(nm, c, n, device)};
+  });
+}
+
+FFB_API int ffcu_dataset_copy_from_host(ffit_dataset* ds, const double* const* cols) {
+  return guarded([&] {
+    require(ds, "dataset");
+    require(cols, "cols");
+    if (!ds->d->owns) ffb::usage_error("cannot refill a view");
+    std::vector<const double*> c(cols, cols + ds->d->cols.size());
+    ds->d->copy_from_host(c);
+  });
+}
+
+FFB_API int ffcu_dataset_slice(const ffit_dataset* ds, long long begin, long long end, ffit_dataset** out) {
+  return guarded([&] {
+    require(ds, "dataset");
+    require(out, "out");
+    if (begin < 0 || end < begin || end > ds->d->n) ffb::usage_error("slice out of range");
+    std::vector<const double*> c;
+    for (double* p : ds->d->cols) c.push_back(p + begin);
+    auto v = ffb::DeviceDataset::view(ds->d->names, c, end - begin, ds->d->device);
+    v->parent = ds->d;
+    *out = new ffit_dataset{std::move(v)};
+  });
+}
+
+FFB_API int ffcu_dataset_ncols(const ffit_dataset* ds) { return static_cast<int>(ds->d->cols.size()); }
+
+FFB_API const char* ffcu_dataset_column_name(const ffit_dataset* ds, int i) {
+  if (i < 0 || i >= static_cast<int>(ds->d->names.size())) return nullptr;
+  return ds->d->names[i].c_str();
+}
+
+FFB_API int ffcu_dataset_download(const ffit_dataset* ds, int col, double* host_out) {
+  return guarded([&] {
+    require(ds, "dataset");
+    require(host_out, "host_out");
+    ds->d->download(col, host_out);
+  });
+}
+
+FFB_API int ffcu_dataset_device_column(const ffit_dataset* ds, int col, const double** dev_ptr) {
+  return guarded([&] {
+    require(ds, "dataset");
+    require(dev_ptr, "dev_ptr");
+    if (col < 0 || col >= static_cast<int>(ds->d->cols.size())) ffb::usage_error("column index out of range");
+    *dev_ptr = ds->d->cols[col];
+  });
+}
+
+// ---------------------------------------------------------------------------
+// fitting
+
+FFB_API int ffit_fit(ffit_model* m, const ffit_dataset* ds, ffit_mode mode, double tolerance,
+                     long max_iterations, ffit_fit_result** out) {
+  return guarded([&] {
+    require(m, "model");
+    require(ds, "dataset");
+    require(out, "out");
+    require_gpu_mode(mode);
+    ffb::FitOptions o;
+    if (tolerance > 0.0) o.tolerance = tolerance;
+    if (max_iterations > 0) o.max_iterations = static_cast<int>(max_iterations);
+    auto r = std::make_unique<ffit_fit_result>();
+    r->r = ffb::fit_nelder_mead(*m->m, engine(m), *ds->d, o);
+    *out = r.release();
+  });
+}
+
+FFB_API int ffcu_fit_gradient(ffit_model* m, const ffit_dataset* ds, double tolerance,
+                              long max_iterations, ffit_fit_result** out) {
+  return guarded([&] {
+    require(m, "model");
+    require(ds, "dataset");
+    require(out, "out");
+    ffb::FitOptions o;
+    o.record_trace = true;
+    if (tolerance > 0.0) o.tolerance = tolerance;
+    if (max_iterations > 0) o.max_iterations = static_cast<int>(max_iterations);
+    auto r = std::make_unique<ffit_fit_result>();
+    r->r = ffb::fit_gradient(*m->m, engine(m), *ds->d, o);
+    *out = r.release();
+  });
+}
+
+FFB_API int ffit_result_converged(const ffit_fit_result* r) { return r->r.converged ? 1 : 0; }
+FFB_API double ffit_result_nll(const ffit_fit_result* r) { return r->r.nll_min; }
+FFB_API unsigned long long ffit_result_nll_calls(const ffit_fit_result* r) { return r->r.n_nll_calls; }
+FFB_API double ffit_result_wall_seconds(const ffit_fit_result* r) { return r->r.wall_seconds; }
+FFB_API int ffit_result_uncertainties_valid(const ffit_fit_result* r) {
+  return r->r.uncertainties_valid ? 1 : 0;
+}
+FFB_API int ffit_result_param_count(const ffit_fit_result* r) {
+  return static_cast<int>(r->r.parameters.size());
+}
+FFB_API const char* ffit_result_param_name(const ffit_fit_result* r, int i) {
+  if (i < 0 || i >= static_cast<int>(r->r.parameters.size())) return nullptr;
+  return r->r.parameters[i].name.c_str();
+}
+FFB_API double ffit_result_param_value(const ffit_fit_result* r, int i) { return r->r.parameters[i].value; }
+FFB_API double ffit_result_param_uncertainty(const ffit_fit_result* r, int i) {
+  return r->r.parameters[i].uncertainty;
+}
+FFB_API void ffit_result_free(ffit_fit_result* r) { delete r; }
+
+FFB_API int ffcu_result_iterations(const ffit_fit_result* r) { return r->r.iterations; }
+FFB_API unsigned long long ffcu_result_launches(const ffit_fit_result* r) { return r->r.n_launches; }
+FFB_API int ffcu_result_trace(const ffit_fit_result* r, double* out, int cap) {
+  const int n = static_cast<int>(r->r.trace.size());
+  for (int i = 0; i < n && i < cap; ++i) out[i] = r->r.trace[i];
+  return n;
+}
+
+// ---------------------------------------------------------------------------
+// instrumentation
+
+FFB_API int ffcu_last_launch(const ffit_model* m, int* info6) {
+  return guarded([&] {
+    require(m, "model");
+    require(info6, "info6");
+    const ffb::NllLaunchInfo i = m->engine->last_launch();
+    info6[0] = i.threads;
+    info6[1] = i.events_per_thread;
+    info6[2] = i.tile;
+    info6[3] = i.ntiles;
+    info6[4] = i.nchunks;
+    info6[5] = i.grid;
+  });
+}
+
+FFB_API unsigned long long ffcu_kernel_launches(void) { return ffb::kernel_launches(); }
+
+FFB_API int ffcu_fp64_peak(double* fma_per_s, float* ms) {
+  return guarded([&] {
+    require(fma_per_s, "fma_per_s");
+    cudaStream_t s;
+    ffb::cuda_check(cudaStreamCreate(&s), "cudaStreamCreate");
+    *fma_per_s = ffb::fp64_peak(s, ms);
+    ffb::cuda_check(cudaGetLastError(), "fp64_peak");
+    cudaStreamDestroy(s);
+    ffb::count_launches(2);
+  });
+}

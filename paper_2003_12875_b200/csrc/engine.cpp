@@ -1,0 +1,330 @@
+#include "engine.hpp"
+
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <limits>
+
+namespace ffb {
+
+namespace {
+
+std::atomic<unsigned long long> g_launches{0};
+constexpr int kMaxPointsPerLaunch = 512;
+
+}  // namespace
+
+unsigned long long kernel_launches() { return g_launches.load(); }
+void count_launches(unsigned long long k) { g_launches += k; }
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    throw Error(ErrorCode::Numeric, std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+  }
+}
+
+DeviceGuard::DeviceGuard(int device) {
+  cuda_check(cudaGetDevice(&prev_), "cudaGetDevice");
+  if (prev_ != device) {
+    cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    switched_ = true;
+  }
+}
+
+DeviceGuard::~DeviceGuard() {
+  if (switched_) cudaSetDevice(prev_);
+}
+
+// ---------------------------------------------------------------------------
+// DeviceDataset
+
+DeviceDataset::~DeviceDataset() {
+  if (owns) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    for (double* c : cols) cudaFree(c);
+    cudaSetDevice(prev);
+  }
+}
+
+int DeviceDataset::column_index(const std::string& name) const {
+  for (std::size_t i = 0; i < names.size(); ++i) {
+    if (names[i] == name) return static_cast<int>(i);
+  }
+  return -1;
+}
+
+std::shared_ptr<DeviceDataset> DeviceDataset::upload(const std::vector<std::string>& names,
+                                                     const std::vector<const double*>& host_cols,
+                                                     long long n) {
+  if (names.size() != host_cols.size()) usage_error("dataset: names/columns length mismatch");
+  if (n < 0) usage_error("dataset: negative row count");
+  for (std::size_t i = 0; i < names.size(); ++i) {
+    for (std::size_t j = 0; j < i; ++j) {
+      if (names[i] == names[j]) data_error("duplicate column name: " + names[i]);
+    }
+  }
+  auto ds = std::make_shared<DeviceDataset>();
+  cuda_check(cudaGetDevice(&ds->device), "cudaGetDevice");
+  ds->n = n;
+  ds->names = names;
+  // Columns are padded to a whole number of 2048-event tiles (16-byte aligned
+  // bulk copies of full tiles; cudaMalloc gives 256-byte alignment).
+  const long long padded = ((n + 2047) / 2048) * 2048 + 2048;
+  for (std::size_t i = 0; i < names.size(); ++i) {
+    double* d = nullptr;
+    cuda_check(cudaMalloc(&d, static_cast<std::size_t>(padded) * sizeof(double)), "cudaMalloc(column)");
+    ds->cols.push_back(d);
+  }
+  ds->copy_from_host(host_cols);
+  return ds;
+}
+
+std::shared_ptr<DeviceDataset> DeviceDataset::view(const std::vector<std::string>& names,
+                                                   const std::vector<const double*>& dev_cols,
+                                                   long long n, int device) {
+  if (names.size() != dev_cols.size()) usage_error("dataset: names/columns length mismatch");
+  auto ds = std::make_shared<DeviceDataset>();
+  ds->device = device;
+  ds->n = n;
+  ds->names = names;
+  ds->owns = false;
+  for (const double* c : dev_cols) {
+    if (!c && n > 0) usage_error("dataset view: null device column");
+    if (reinterpret_cast<uintptr_t>(c) % 8 != 0) usage_error("dataset view: columns must be 8-byte aligned");
+    ds->cols.push_back(const_cast<double*>(c));
+  }
+  return ds;
+}
+
+void DeviceDataset::copy_from_host(const std::vector<const double*>& host_cols) {
+  if (host_cols.size() != cols.size()) usage_error("dataset: column count mismatch");
+  if (n == 0) return;
+  DeviceGuard g(device);
+  for (std::size_t i = 0; i < cols.size(); ++i) {
+    if (!host_cols[i]) usage_error("dataset: null host column");
+    cuda_check(cudaMemcpy(cols[i], host_cols[i], static_cast<std::size_t>(n) * sizeof(double),
+                          cudaMemcpyHostToDevice),
+               "cudaMemcpy(H2D column)");
+  }
+}
+
+void DeviceDataset::download(int col, double* host_out) const {
+  if (col < 0 || col >= static_cast<int>(cols.size())) usage_error("dataset: column index out of range");
+  if (n == 0) return;
+  DeviceGuard g(device);
+  cuda_check(cudaMemcpy(host_out, cols[col], static_cast<std::size_t>(n) * sizeof(double),
+                        cudaMemcpyDeviceToHost),
+             "cudaMemcpy(D2H column)");
+}
+
+// ---------------------------------------------------------------------------
+// Engine
+
+Engine::Engine(const Model& m) : m_(m), plan_(compile_plan(m, m.root, true)) {}
+
+Engine::~Engine() {
+  if (device_ >= 0) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device_);
+    for (int k = 0; k < 2; ++k) {
+      cudaFree(d_consts_[k]);
+      cudaFreeHost(h_consts_[k]);
+      if (staged_[k]) cudaEventDestroy(staged_[k]);
+    }
+    cudaFree(d_scratch_);
+    cudaFree(d_pairs_);
+    cudaFree(d_bad_);
+    cudaFreeHost(h_pairs_);
+    cudaFreeHost(h_bad_);
+    if (stream_) cudaStreamDestroy(stream_);
+    cudaSetDevice(prev);
+  }
+}
+
+cudaStream_t Engine::stream(int device) {
+  ensure(device, 1, 0);
+  return stream_;
+}
+
+void Engine::ensure(int device, int P, std::size_t scratch) {
+  if (device_ != device) {
+    if (device_ >= 0) usage_error("a model's GPU engine is bound to one device; use one model per device");
+    device_ = device;
+    cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+    for (int k = 0; k < 2; ++k) {
+      cuda_check(cudaEventCreateWithFlags(&staged_[k], cudaEventDisableTiming), "cudaEventCreate");
+    }
+  }
+  if (P > cap_points_) {
+    const int cap = std::max(P, 16);
+    for (int k = 0; k < 2; ++k) {
+      cuda_check(cudaEventSynchronize(staged_[k]), "cudaEventSynchronize");
+      cudaFree(d_consts_[k]);
+      cudaFreeHost(h_consts_[k]);
+    }
+    cuda_check(cudaStreamSynchronize(stream_), "cudaStreamSynchronize");
+    cudaFree(d_pairs_);
+    cudaFree(d_bad_);
+    cudaFreeHost(h_pairs_);
+    cudaFreeHost(h_bad_);
+    const std::size_t cbytes = static_cast<std::size_t>(cap) * std::max(1, plan_.dev.stride) * sizeof(double);
+    for (int k = 0; k < 2; ++k) {
+      cuda_check(cudaMalloc(&d_consts_[k], cbytes), "cudaMalloc(consts)");
+      cuda_check(cudaHostAlloc(&h_consts_[k], cbytes, cudaHostAllocDefault), "cudaHostAlloc(consts)");
+    }
+    cuda_check(cudaMalloc(&d_pairs_, cap * sizeof(SumPair)), "cudaMalloc(pairs)");
+    cuda_check(cudaMalloc(&d_bad_, cap * sizeof(unsigned long long)), "cudaMalloc(bad)");
+    cuda_check(cudaHostAlloc(&h_pairs_, cap * sizeof(SumPair), cudaHostAllocDefault), "cudaHostAlloc");
+    cuda_check(cudaHostAlloc(&h_bad_, cap * sizeof(unsigned long long), cudaHostAllocDefault), "cudaHostAlloc");
+    cap_points_ = cap;
+  }
+  if (scratch > cap_scratch_) {
+    cuda_check(cudaStreamSynchronize(stream_), "cudaStreamSynchronize");
+    cudaFree(d_scratch_);
+    cuda_check(cudaMalloc(&d_scratch_, scratch), "cudaMalloc(scratch)");
+    cap_scratch_ = scratch;
+  }
+}
+
+void Engine::bind_columns(const HostPlan& plan, const DeviceDataset& ds, ColPtrs& cols) const {
+  std::memset(&cols, 0, sizeof(cols));
+  for (std::size_t s = 0; s < plan.col_obs.size(); ++s) {
+    const std::string& name = m_.observables[plan.col_obs[s]].name;
+    const int ci = ds.column_index(name);
+    if (ci < 0) data_error("unknown column: " + name);
+    cols.c[s] = ds.cols[ci];
+  }
+}
+
+const double* Engine::upload_constants(const HostPlan& plan, const double* thetas, int P,
+                                       cudaStream_t s) {
+  const int k = slot_ ^= 1;
+  // slot k fed the copy two calls ago; that copy must be done before reuse
+  cuda_check(cudaEventSynchronize(staged_[k]), "cudaEventSynchronize");
+  const int npar = static_cast<int>(m_.params.size());
+  const int stride = plan.dev.stride;
+  for (int p = 0; p < P; ++p) {
+    build_constants(plan, m_, thetas + static_cast<std::size_t>(p) * npar,
+                    h_consts_[k] + static_cast<std::size_t>(p) * stride);
+  }
+  cuda_check(cudaMemcpyAsync(d_consts_[k], h_consts_[k],
+                             static_cast<std::size_t>(P) * stride * sizeof(double),
+                             cudaMemcpyHostToDevice, s),
+             "cudaMemcpyAsync(consts)");
+  cuda_check(cudaEventRecord(staged_[k], s), "cudaEventRecord");
+  return d_consts_[k];
+}
+
+int Engine::nll_points_device(const DeviceDataset& ds, const double* thetas, int P,
+                              SumPair* d_pairs, unsigned long long* d_bad, cudaStream_t stream) {
+  if (P <= 0) return 0;
+  if (P > kMaxPointsPerLaunch) usage_error("nll_points_device: at most 512 points per call");
+  DeviceGuard g(ds.device);
+  const std::size_t scratch = ds.n > 0 ? nll_scratch_bytes(ds.n, P, plan_.dev.ncols) : 0;
+  ensure(ds.device, P, scratch);
+  cudaStream_t s = stream ? stream : stream_;
+  if (s != stream_) {
+    // order this call after the engine's previous work and vice versa
+    cudaEvent_t ev;
+    cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
+    cudaEventRecord(ev, stream_);
+    cudaStreamWaitEvent(s, ev, 0);
+    cudaEventDestroy(ev);
+  }
+  const double* d_consts = upload_constants(plan_, thetas, P, s);
+  int launches = 0;
+  if (ds.n == 0) {
+    cuda_check(cudaMemsetAsync(d_pairs, 0, P * sizeof(SumPair), s), "cudaMemsetAsync");
+    cuda_check(cudaMemsetAsync(d_bad, 0xff, P * sizeof(unsigned long long), s), "cudaMemsetAsync");
+  } else {
+    ColPtrs cols;
+    bind_columns(plan_, ds, cols);
+    last_ = launch_nll(plan_.dev, cols, ds.n, d_consts, P, d_scratch_, d_pairs, d_bad, s);
+    launches = last_.launches;
+    cuda_check(cudaGetLastError(), "launch_nll");
+  }
+  if (s != stream_) {
+    cudaEvent_t ev;
+    cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
+    cudaEventRecord(ev, s);
+    cudaStreamWaitEvent(stream_, ev, 0);
+    cudaEventDestroy(ev);
+  }
+  count_launches(launches);
+  return launches;
+}
+
+NllResult Engine::nll_points(const DeviceDataset& ds, const double* thetas, int P) {
+  NllResult r;
+  r.value.resize(P);
+  r.pairs.resize(P);
+  r.first_invalid.resize(P);
+  const int npar = static_cast<int>(m_.params.size());
+  DeviceGuard g(ds.device);
+  for (int p0 = 0; p0 < P; p0 += kMaxPointsPerLaunch) {
+    const int np = std::min(kMaxPointsPerLaunch, P - p0);
+    const double* th = thetas + static_cast<std::size_t>(p0) * npar;
+    ensure(ds.device, np, 0);
+    r.launches += nll_points_device(ds, th, np, d_pairs_, d_bad_, stream_);
+    cuda_check(cudaMemcpyAsync(h_pairs_, d_pairs_, np * sizeof(SumPair), cudaMemcpyDeviceToHost, stream_),
+               "cudaMemcpyAsync(pairs)");
+    cuda_check(cudaMemcpyAsync(h_bad_, d_bad_, np * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                               stream_),
+               "cudaMemcpyAsync(bad)");
+    cuda_check(cudaStreamSynchronize(stream_), "nll kernels");
+    for (int i = 0; i < np; ++i) {
+      const int p = p0 + i;
+      r.pairs[p] = h_pairs_[i];
+      const bool bad = h_bad_[i] != kNoInvalid;
+      r.first_invalid[p] = bad ? static_cast<long long>(h_bad_[i]) : -1;
+      r.value[p] = bad ? std::numeric_limits<double>::infinity()
+                       : (h_pairs_[i].s + h_pairs_[i].c) +
+                             m_.extended_term(th + static_cast<std::size_t>(i) * npar,
+                                              static_cast<double>(ds.n));
+    }
+  }
+  return r;
+}
+
+void Engine::probabilities(const DeviceDataset& ds, const double* theta, double* out,
+                           bool out_on_device, cudaStream_t stream) {
+  eval_batch(-1, ds, theta, out, out_on_device, stream);
+}
+
+void Engine::eval_batch(int pdf, const DeviceDataset& ds, const double* theta, double* out,
+                        bool out_on_device, cudaStream_t stream) {
+  const HostPlan plan = pdf < 0 ? plan_ : compile_plan(m_, pdf, false);
+  m_.check_params(plan.pdf, theta);
+  if (ds.n == 0) return;
+  DeviceGuard g(ds.device);
+  ensure(ds.device, 1, 0);
+  cudaStream_t s = stream ? stream : stream_;
+  ColPtrs cols;
+  bind_columns(plan, ds, cols);
+  if (s != stream_) cuda_check(cudaStreamSynchronize(stream_), "cudaStreamSynchronize");
+  const double* d_consts = upload_constants(plan, theta, 1, s);
+  double* d_out = out;
+  if (!out_on_device) {
+    cuda_check(cudaMalloc(&d_out, static_cast<std::size_t>(ds.n) * sizeof(double)), "cudaMalloc(out)");
+  }
+  count_launches(launch_eval(plan.dev, cols, ds.n, d_consts, d_out, s));
+  cuda_check(cudaGetLastError(), "launch_eval");
+  if (!out_on_device) {
+    cuda_check(cudaMemcpyAsync(out, d_out, static_cast<std::size_t>(ds.n) * sizeof(double),
+                               cudaMemcpyDeviceToHost, s),
+               "cudaMemcpyAsync(out)");
+    cuda_check(cudaStreamSynchronize(s), "eval kernel");
+    cudaFree(d_out);
+  } else if (s != stream_) {
+    cudaEvent_t ev;
+    cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
+    cudaEventRecord(ev, s);
+    cudaStreamWaitEvent(stream_, ev, 0);
+    cudaEventDestroy(ev);
+  }
+}
+
+}  // namespace ffb

@@ -1,0 +1,124 @@
+// Host orchestration of the GPU likelihood: HBM-resident SoA datasets and the
+// per-model engine that builds per-point constants, uploads them and launches
+// the fused kernels.  This is where the reference's nll_batch / probabilities /
+// eval_batch (proj/src/eval.cpp:119-192, proj/src/pdfs.cpp:212-269) cross to the
+// device.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "model.hpp"
+#include "plan_build.hpp"
+
+namespace ffb {
+
+// Immutable SoA event table resident in HBM: one contiguous fp64 column per
+// observable (the reference's DataSet, proj/include/ffit/dataset.hpp:20-51).
+struct DeviceDataset {
+  int device = 0;
+  long long n = 0;
+  std::vector<std::string> names;
+  std::vector<double*> cols;
+  bool owns = true;
+  std::shared_ptr<DeviceDataset> parent;  // keeps the storage of a view alive
+
+  DeviceDataset() = default;
+  DeviceDataset(const DeviceDataset&) = delete;
+  DeviceDataset& operator=(const DeviceDataset&) = delete;
+  ~DeviceDataset();
+
+  int column_index(const std::string& name) const;  // -1 if absent
+
+  static std::shared_ptr<DeviceDataset> upload(const std::vector<std::string>& names,
+                                               const std::vector<const double*>& host_cols,
+                                               long long n);
+  static std::shared_ptr<DeviceDataset> view(const std::vector<std::string>& names,
+                                             const std::vector<const double*>& dev_cols,
+                                             long long n, int device);
+  void copy_from_host(const std::vector<const double*>& host_cols);
+  void download(int col, double* host_out) const;
+};
+
+void cuda_check(cudaError_t e, const char* what);
+
+class DeviceGuard {
+ public:
+  explicit DeviceGuard(int device);
+  ~DeviceGuard();
+
+ private:
+  int prev_ = 0;
+  bool switched_ = false;
+};
+
+struct NllResult {
+  std::vector<double> value;         // s + c + extended term; +inf if an event is invalid
+  std::vector<SumPair> pairs;        // the raw per-point Neumaier pairs (events only)
+  std::vector<long long> first_invalid;
+  unsigned long long launches = 0;
+};
+
+class Engine {
+ public:
+  explicit Engine(const Model& m);
+  ~Engine();
+  Engine(const Engine&) = delete;
+  Engine& operator=(const Engine&) = delete;
+
+  // Synchronous: P points (rows of all model parameters, declaration order).
+  NllResult nll_points(const DeviceDataset& ds, const double* thetas, int P);
+
+  // Asynchronous on `stream`: results stay on the device (d_pairs: P pairs,
+  // d_bad: P indices, kNoInvalid if none).  Host-side constant building and the
+  // constant upload are part of the call.  Returns kernels launched.
+  int nll_points_device(const DeviceDataset& ds, const double* thetas, int P, SumPair* d_pairs,
+                        unsigned long long* d_bad, cudaStream_t stream);
+
+  // probabilities() (proj/src/eval.cpp:174-192): normalised per-event values.
+  void probabilities(const DeviceDataset& ds, const double* theta, double* out, bool out_on_device,
+                     cudaStream_t stream = nullptr);
+
+  // PdfSpec::eval_batch (proj/src/pdfs.cpp:212-269): unnormalised values of a
+  // (sub-)pdf of the model.
+  void eval_batch(int pdf, const DeviceDataset& ds, const double* theta, double* out,
+                  bool out_on_device, cudaStream_t stream = nullptr);
+
+  const HostPlan& likelihood_plan() const { return plan_; }
+  NllLaunchInfo last_launch() const { return last_; }
+  cudaStream_t stream(int device);
+
+ private:
+  void bind_columns(const HostPlan& plan, const DeviceDataset& ds, ColPtrs& cols) const;
+  void ensure(int device, int P, std::size_t scratch);
+  const double* upload_constants(const HostPlan& plan, const double* thetas, int P, cudaStream_t s);
+
+  const Model& m_;
+  HostPlan plan_;
+  int device_ = -1;
+  cudaStream_t stream_ = nullptr;
+  int cap_points_ = 0;
+  std::size_t cap_scratch_ = 0;
+  // double-buffered constant rows: host builds slot k while the GPU may still
+  // be copying / reading slot k^1
+  double* d_consts_[2] = {nullptr, nullptr};
+  double* h_consts_[2] = {nullptr, nullptr};  // pinned
+  cudaEvent_t staged_[2] = {nullptr, nullptr};
+  int slot_ = 0;
+  void* d_scratch_ = nullptr;
+  SumPair* d_pairs_ = nullptr;
+  unsigned long long* d_bad_ = nullptr;
+  SumPair* h_pairs_ = nullptr;             // pinned
+  unsigned long long* h_bad_ = nullptr;    // pinned
+  NllLaunchInfo last_{};
+};
+
+// Process-wide count of kernels this library launched.
+unsigned long long kernel_launches();
+void count_launches(unsigned long long k);
+
+}  // namespace ffb

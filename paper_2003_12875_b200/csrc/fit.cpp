@@ -1,0 +1,388 @@
+#include "fit.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <limits>
+#include <numeric>
+
+namespace ffb {
+
+double bound_transform(double u, double lower, double upper) {
+  return lower + (upper - lower) * (std::sin(u) + 1.0) * 0.5;  // proj/src/fit.cpp:12-14
+}
+
+double bound_transform_inverse(double p, double lower, double upper) {
+  if (!(p > lower && p < upper)) {
+    numeric_error("bound_transform_inverse: value " + std::to_string(p) + " not strictly inside (" +
+                  std::to_string(lower) + ", " + std::to_string(upper) + ")");
+  }
+  return std::asin(2.0 * (p - lower) / (upper - lower) - 1.0);
+}
+
+namespace {
+
+constexpr double kHalfPi = 1.5707963267948966;
+
+// The objective over u-space points, evaluated in batches: one call = one
+// multi-point GPU launch (the reference's Objective, proj/src/fit.cpp:30-49,
+// evaluates one point per nll() call).
+struct BatchObjective {
+  Model& m;
+  Engine& e;
+  const DeviceDataset& ds;
+  std::vector<int> free_ids;
+  unsigned long long calls = 0, batches = 0, kernels = 0;
+
+  std::vector<double> theta_of(const std::vector<double>& u) const {
+    std::vector<double> th = m.theta();
+    for (std::size_t i = 0; i < free_ids.size(); ++i) {
+      const Parameter& p = m.params[free_ids[i]];
+      const double v = bound_transform(u[i], p.lo, p.hi);
+      if (!(p.lo <= v && v <= p.hi)) {  // Graph::set_value, proj/src/graph.cpp:121-124
+        numeric_error("set_value: " + std::to_string(v) + " outside range of '" + p.name + "'");
+      }
+      th[free_ids[i]] = v;
+    }
+    return th;
+  }
+
+  std::vector<double> operator()(const std::vector<std::vector<double>>& us) {
+    const std::size_t npar = m.params.size();
+    std::vector<double> rows(us.size() * npar);
+    for (std::size_t k = 0; k < us.size(); ++k) {
+      const std::vector<double> th = theta_of(us[k]);
+      std::copy(th.begin(), th.end(), rows.begin() + static_cast<std::ptrdiff_t>(k * npar));
+    }
+    const NllResult r = e.nll_points(ds, rows.data(), static_cast<int>(us.size()));
+    calls += us.size();
+    batches += 1;
+    kernels += r.launches;
+    return r.value;
+  }
+
+  double one(const std::vector<double>& u) { return (*this)({u})[0]; }
+
+  void apply(const std::vector<double>& u) {
+    const std::vector<double> th = theta_of(u);
+    for (const int id : free_ids) m.params[id].value = th[id];
+  }
+};
+
+// Gauss-Jordan with partial pivoting (proj/src/fit.cpp:53-84).
+bool invert(std::vector<std::vector<double>>& a) {
+  const std::size_t n = a.size();
+  std::vector<std::vector<double>> inv(n, std::vector<double>(n, 0.0));
+  for (std::size_t i = 0; i < n; ++i) inv[i][i] = 1.0;
+  for (std::size_t col = 0; col < n; ++col) {
+    std::size_t pivot = col;
+    for (std::size_t r = col + 1; r < n; ++r) {
+      if (std::fabs(a[r][col]) > std::fabs(a[pivot][col])) pivot = r;
+    }
+    if (!(std::fabs(a[pivot][col]) > 0.0) || !std::isfinite(a[pivot][col])) return false;
+    std::swap(a[col], a[pivot]);
+    std::swap(inv[col], inv[pivot]);
+    const double d = a[col][col];
+    for (std::size_t c = 0; c < n; ++c) {
+      a[col][c] /= d;
+      inv[col][c] /= d;
+    }
+    for (std::size_t r = 0; r < n; ++r) {
+      if (r == col) continue;
+      const double f = a[r][col];
+      if (f == 0.0) continue;
+      for (std::size_t c = 0; c < n; ++c) {
+        a[r][c] -= f * a[col][c];
+        inv[r][c] -= f * inv[col][c];
+      }
+    }
+  }
+  a = std::move(inv);
+  return true;
+}
+
+std::vector<double> start_u(const Model& m, const std::vector<int>& free_ids) {
+  std::vector<double> u(free_ids.size());
+  for (std::size_t i = 0; i < free_ids.size(); ++i) {
+    const Parameter& p = m.params[free_ids[i]];
+    u[i] = bound_transform_inverse(p.value, p.lo, p.hi);
+  }
+  return u;
+}
+
+// Hessian points exactly as proj/src/fit.cpp:200-225 builds them (same
+// floating-point operation sequence), evaluated as one batch.
+bool hessian_at(BatchObjective& f, const std::vector<double>& u_min, double h,
+                std::vector<std::vector<double>>& hess) {
+  const std::size_t dim = u_min.size();
+  std::vector<std::vector<double>> pts;
+  pts.push_back(u_min);
+  for (std::size_t i = 0; i < dim; ++i) {
+    std::vector<double> up = u_min;
+    up[i] = u_min[i] + h;
+    pts.push_back(up);
+    up[i] = u_min[i] - h;
+    pts.push_back(up);
+    for (std::size_t j = i + 1; j < dim; ++j) {
+      up = u_min;
+      up[i] += h;
+      up[j] += h;
+      pts.push_back(up);  // fpp
+      up[j] -= 2.0 * h;
+      pts.push_back(up);  // fpm
+      up[i] -= 2.0 * h;
+      pts.push_back(up);  // fmm
+      up[j] += 2.0 * h;
+      pts.push_back(up);  // fmp
+    }
+  }
+  const std::vector<double> v = f(pts);
+  hess.assign(dim, std::vector<double>(dim, 0.0));
+  const double f0 = v[0];
+  std::size_t k = 1;
+  for (std::size_t i = 0; i < dim; ++i) {
+    const double fp = v[k++], fm = v[k++];
+    hess[i][i] = (fp - 2.0 * f0 + fm) / (h * h);
+    for (std::size_t j = i + 1; j < dim; ++j) {
+      const double fpp = v[k++], fpm = v[k++], fmm = v[k++], fmp = v[k++];
+      hess[i][j] = hess[j][i] = (fpp - fpm - fmp + fmm) / (4.0 * h * h);
+    }
+  }
+  return invert(hess);
+}
+
+void finish(Model& m, BatchObjective& f, const std::vector<double>& u_min, double h, FitResult& r) {
+  std::vector<std::vector<double>> hess;
+  const bool invertible = hessian_at(f, u_min, h, hess);
+  f.apply(u_min);  // leave the model in the fitted state (proj/src/fit.cpp:228-229)
+  r.uncertainties_valid = invertible;
+  r.parameters.clear();
+  for (std::size_t i = 0; i < f.free_ids.size(); ++i) {
+    Parameter& p = m.params[f.free_ids[i]];
+    FittedParameter fp;
+    fp.name = p.name;
+    fp.value = p.value;
+    if (invertible && hess[i][i] > 0.0) {
+      const double jac = 0.5 * (p.hi - p.lo) * std::fabs(std::cos(u_min[i]));
+      fp.uncertainty = std::sqrt(hess[i][i]) * jac;
+    } else {
+      fp.uncertainty = 0.0;
+      r.uncertainties_valid = false;
+    }
+    p.error = fp.uncertainty;
+    r.parameters.push_back(fp);
+  }
+}
+
+void validate(const Model& m, const FitOptions& o, const std::vector<int>& free_ids) {
+  if (!(o.tolerance > 0.0) || o.max_iterations <= 0) usage_error("invalid fit options");
+  if (free_ids.empty()) usage_error("fit requires at least one non-constant parameter");
+  const std::vector<double> th = m.theta();
+  m.check_params(m.root, th.data());
+}
+
+}  // namespace
+
+FitResult fit_nelder_mead(Model& m, Engine& e, const DeviceDataset& ds, const FitOptions& o) {
+  const auto t0 = std::chrono::steady_clock::now();
+  BatchObjective f{m, e, ds, m.free_parameters()};
+  validate(m, o, f.free_ids);
+  const std::size_t dim = f.free_ids.size();
+  const std::vector<double> u0 = start_u(m, f.free_ids);
+
+  // initial simplex (proj/src/fit.cpp:108-123): u0 and d offset vertices, one batch
+  std::vector<std::vector<double>> simplex(dim + 1, u0);
+  for (std::size_t i = 0; i < dim; ++i) {
+    double step = 0.1 * (kHalfPi - u0[i]);
+    if (step < 1e-3) step = -0.1 * (u0[i] + kHalfPi);
+    simplex[i + 1][i] += step;
+  }
+  std::vector<double> fv = f(simplex);
+  if (!std::isfinite(fv[0])) {
+    numeric_error("NLL is not finite at the starting parameters (zero-probability entry)");
+  }
+
+  FitResult result;
+  std::vector<std::size_t> order(dim + 1);
+  std::vector<double> centroid(dim), xr(dim), xe(dim), xc(dim);
+  bool converged = false;
+  int iter = 0;
+  for (; iter < o.max_iterations; ++iter) {  // proj/src/fit.cpp:130-190
+    std::iota(order.begin(), order.end(), std::size_t{0});
+    std::stable_sort(order.begin(), order.end(), [&](std::size_t a, std::size_t b) { return fv[a] < fv[b]; });
+    const std::size_t best = order.front();
+    const std::size_t worst = order.back();
+    const std::size_t second_worst = order[dim - 1];
+    if (o.record_trace) result.trace.push_back(fv[best]);
+    if (fv[worst] - fv[best] < o.tolerance) {
+      converged = true;
+      break;
+    }
+    for (std::size_t i = 0; i < dim; ++i) {
+      double s = 0.0;
+      for (std::size_t v = 0; v <= dim; ++v) {
+        if (v != worst) s += simplex[v][i];
+      }
+      centroid[i] = s / static_cast<double>(dim);
+    }
+    for (std::size_t i = 0; i < dim; ++i) xr[i] = centroid[i] + (centroid[i] - simplex[worst][i]);
+    const double fr = f.one(xr);
+    if (fr < fv[best]) {
+      for (std::size_t i = 0; i < dim; ++i) xe[i] = centroid[i] + 2.0 * (centroid[i] - simplex[worst][i]);
+      const double fe = f.one(xe);
+      if (fe < fr) {
+        simplex[worst] = xe;
+        fv[worst] = fe;
+      } else {
+        simplex[worst] = xr;
+        fv[worst] = fr;
+      }
+    } else if (fr < fv[second_worst]) {
+      simplex[worst] = xr;
+      fv[worst] = fr;
+    } else {
+      const bool outside = fr < fv[worst];
+      if (outside) {
+        for (std::size_t i = 0; i < dim; ++i) xc[i] = centroid[i] + 0.5 * (xr[i] - centroid[i]);
+      } else {
+        for (std::size_t i = 0; i < dim; ++i) xc[i] = centroid[i] + 0.5 * (simplex[worst][i] - centroid[i]);
+      }
+      const double fc = f.one(xc);
+      if (fc < std::min(fr, fv[worst])) {
+        simplex[worst] = xc;
+        fv[worst] = fc;
+      } else {  // shrink: d independent points, one batch
+        std::vector<std::size_t> idx;
+        std::vector<std::vector<double>> pts;
+        for (std::size_t v = 0; v <= dim; ++v) {
+          if (v == best) continue;
+          for (std::size_t i = 0; i < dim; ++i) {
+            simplex[v][i] = simplex[best][i] + 0.5 * (simplex[v][i] - simplex[best][i]);
+          }
+          idx.push_back(v);
+          pts.push_back(simplex[v]);
+        }
+        const std::vector<double> vals = f(pts);
+        for (std::size_t k = 0; k < idx.size(); ++k) fv[idx[k]] = vals[k];
+      }
+    }
+  }
+  std::size_t best = 0;
+  for (std::size_t v = 1; v <= dim; ++v) {
+    if (fv[v] < fv[best]) best = v;
+  }
+  result.converged = converged;
+  result.nll_min = fv[best];
+  result.iterations = iter;
+  finish(m, f, simplex[best], o.fd_step, result);
+  result.n_nll_calls = f.calls;
+  result.n_launches = f.batches;
+  result.kernel_launches = f.kernels;
+  result.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return result;
+}
+
+FitResult fit_gradient(Model& m, Engine& e, const DeviceDataset& ds, const FitOptions& o) {
+  const auto t0 = std::chrono::steady_clock::now();
+  BatchObjective f{m, e, ds, m.free_parameters()};
+  validate(m, o, f.free_ids);
+  const std::size_t d = f.free_ids.size();
+  const double h = o.fd_step;
+  std::vector<double> u = start_u(m, f.free_ids);
+  std::vector<double> u_prev, g_prev, u_best = u;
+  std::vector<std::vector<double>> H(d, std::vector<double>(d, 0.0));
+  double f_prev = std::numeric_limits<double>::infinity(), f_best = f_prev;
+  bool have_prev = false, converged = false;
+  int backtracks = 0, iter = 0;
+  FitResult result;
+  for (; iter < o.max_iterations; ++iter) {
+    // one launch: the centre and the 2d central-difference points
+    std::vector<std::vector<double>> pts(1, u);
+    for (std::size_t i = 0; i < d; ++i) {
+      std::vector<double> a = u, b = u;
+      a[i] += h;
+      b[i] -= h;
+      pts.push_back(a);
+      pts.push_back(b);
+    }
+    const std::vector<double> v = f(pts);
+    const double f0 = v[0];
+    if (!std::isfinite(f0) || (have_prev && f0 > f_prev)) {
+      if (!have_prev) numeric_error("NLL is not finite at the starting parameters (zero-probability entry)");
+      if (++backtracks > 40) break;
+      for (std::size_t i = 0; i < d; ++i) u[i] = u_prev[i] + 0.5 * (u[i] - u_prev[i]);
+      continue;
+    }
+    backtracks = 0;
+    if (o.record_trace) result.trace.push_back(f0);
+    if (f0 < f_best) {
+      f_best = f0;
+      u_best = u;
+    }
+    std::vector<double> g(d), curv(d);
+    for (std::size_t i = 0; i < d; ++i) {
+      g[i] = (v[1 + 2 * i] - v[2 + 2 * i]) / (2.0 * h);
+      curv[i] = (v[1 + 2 * i] - 2.0 * f0 + v[2 + 2 * i]) / (h * h);
+    }
+    if (!have_prev) {
+      for (std::size_t i = 0; i < d; ++i) H[i][i] = curv[i] > 0.0 ? 1.0 / curv[i] : 1e-2;
+    } else {  // BFGS update of the inverse Hessian
+      std::vector<double> s(d), y(d);
+      double sy = 0.0;
+      for (std::size_t i = 0; i < d; ++i) {
+        s[i] = u[i] - u_prev[i];
+        y[i] = g[i] - g_prev[i];
+        sy += s[i] * y[i];
+      }
+      if (sy > 0.0) {
+        const double rho = 1.0 / sy;
+        std::vector<double> Hy(d, 0.0);
+        for (std::size_t i = 0; i < d; ++i) {
+          for (std::size_t j = 0; j < d; ++j) Hy[i] += H[i][j] * y[j];
+        }
+        double yHy = 0.0;
+        for (std::size_t i = 0; i < d; ++i) yHy += y[i] * Hy[i];
+        for (std::size_t i = 0; i < d; ++i) {
+          for (std::size_t j = 0; j < d; ++j) {
+            H[i][j] += (1.0 + rho * yHy) * rho * s[i] * s[j] - rho * (Hy[i] * s[j] + s[i] * Hy[j]);
+          }
+        }
+      }
+    }
+    double edm = 0.0;
+    std::vector<double> step(d, 0.0);
+    for (std::size_t i = 0; i < d; ++i) {
+      for (std::size_t j = 0; j < d; ++j) step[i] -= H[i][j] * g[j];
+      edm -= 0.5 * g[i] * step[i];
+    }
+    if (edm < o.tolerance && have_prev) {
+      converged = true;
+      break;
+    }
+    u_prev = u;
+    g_prev = g;
+    f_prev = f0;
+    have_prev = true;
+    for (std::size_t i = 0; i < d; ++i) u[i] += step[i];
+  }
+  result.converged = converged;
+  result.nll_min = f_best;
+  result.iterations = iter;
+  finish(m, f, u_best, h, result);
+  result.n_nll_calls = f.calls;
+  result.n_launches = f.batches;
+  result.kernel_launches = f.kernels;
+  result.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return result;
+}
+
+bool hessian_uncertainties(Model& m, Engine& e, const DeviceDataset& ds, double h, FitResult& r) {
+  BatchObjective f{m, e, ds, m.free_parameters()};
+  if (f.free_ids.empty()) usage_error("no free parameters");
+  finish(m, f, start_u(m, f.free_ids), h, r);
+  r.n_nll_calls += f.calls;
+  r.n_launches += f.batches;
+  return r.uncertainties_valid;
+}
+
+}  // namespace ffb

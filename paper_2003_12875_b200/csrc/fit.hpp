@@ -1,0 +1,54 @@
+// Fit drivers on top of the GPU likelihood.
+//
+//  * fit_nelder_mead: the reference minimiser (proj/src/fit.cpp:86-251, Nelder-Mead
+//    in sine-transformed space, central-difference Hessian) with every batch of
+//    independent points -- the initial simplex, a shrink, the 1+2d+2d(d-1) Hessian
+//    points -- issued as ONE multi-point launch.
+//  * fit_gradient: Minuit-style quasi-Newton (BFGS on central finite-difference
+//    gradients); each iteration is one launch of 2d+1 points.
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include "engine.hpp"
+
+namespace ffb {
+
+struct FitOptions {
+  double tolerance = 1e-8;  // NM: simplex NLL spread; gradient: EDM threshold
+  int max_iterations = 10000;
+  bool record_trace = false;
+  double fd_step = 1e-4;    // u-space step for gradients / Hessian
+};
+
+struct FittedParameter {
+  std::string name;
+  double value = 0.0;
+  double uncertainty = 0.0;
+};
+
+struct FitResult {
+  bool converged = false;
+  double nll_min = 0.0;
+  std::vector<FittedParameter> parameters;
+  unsigned long long n_nll_calls = 0;   // parameter points evaluated
+  unsigned long long n_launches = 0;    // multi-point launches (batches)
+  unsigned long long kernel_launches = 0;
+  int iterations = 0;
+  double wall_seconds = 0.0;
+  bool uncertainties_valid = true;
+  std::vector<double> trace;
+};
+
+double bound_transform(double u, double lower, double upper);
+double bound_transform_inverse(double p, double lower, double upper);
+
+FitResult fit_nelder_mead(Model& m, Engine& e, const DeviceDataset& ds, const FitOptions& o);
+FitResult fit_gradient(Model& m, Engine& e, const DeviceDataset& ds, const FitOptions& o);
+
+// Central-difference Hessian in u-space at the model's current values (one
+// launch of 1+2d+2d(d-1) points) -> uncertainties written into the model.
+bool hessian_uncertainties(Model& m, Engine& e, const DeviceDataset& ds, double h, FitResult& r);
+
+}  // namespace ffb

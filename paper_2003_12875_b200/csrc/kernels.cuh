@@ -1,0 +1,61 @@
+// Launch interface of the sm_100a kernels (kernels.cu).  All launches are
+// asynchronous on the given stream and return the number of kernels launched
+// (the reference's batch-mode call accounting, proj/include/ffit/eval.hpp:14-21:
+// independent of the number of events).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "plan.hpp"
+
+namespace ffb {
+
+struct ColPtrs {
+  const double* c[kMaxCols];
+};
+
+// Neumaier pair per parameter point (value = s + c).
+struct SumPair {
+  double s, c;
+};
+
+constexpr unsigned long long kNoInvalid = ~0ull;
+
+struct NllLaunchInfo {
+  int threads = 0;
+  int events_per_thread = 0;
+  int tile = 0;
+  int ntiles = 0;
+  int nchunks = 0;
+  int grid = 0;
+  int launches = 0;
+};
+
+// Bytes of scratch the fused NLL launch needs for (n events, P points).
+std::size_t nll_scratch_bytes(long long n, int P, int ncols);
+
+// Fused likelihood: for every point p in [0, P) and every event i in [0, n):
+//   v = -log(plan(x_i; consts[p])) summed with compensated (Neumaier) block
+//   partials, then a deterministic fixed-order pass over the partials.
+// out[p] = (s, c) with NLL_events(p) = s + c; bad[p] = smallest event index with
+// p <= 0 or non-finite (kNoInvalid if none).  `scratch` holds nll_scratch_bytes.
+NllLaunchInfo launch_nll(const DevPlan& plan, const ColPtrs& cols, long long n,
+                         const double* d_consts, int P, void* scratch, SumPair* d_out,
+                         unsigned long long* d_bad, cudaStream_t stream);
+
+// Per-event values of the plan for one point (probabilities() when the plan is
+// normalised, PdfSpec::eval_batch when not).
+int launch_eval(const DevPlan& plan, const ColPtrs& cols, long long n, const double* d_consts,
+                double* d_out, cudaStream_t stream);
+
+// Combine R per-rank Neumaier pairs per point in fixed rank order (multi-GPU
+// exchange step after an all-gather): in = R x P pairs, out = P pairs.
+int launch_combine_ranks(const SumPair* d_in, int R, int P, SumPair* d_out, cudaStream_t stream);
+
+// DFMA-chain microbenchmark: returns FP64 FMA instructions per second measured
+// with CUDA events on `stream` (the FP64 roofline denominator).
+double fp64_peak(cudaStream_t stream, float* ms_out);
+
+}  // namespace ffb

@@ -1,0 +1,52 @@
+// Evaluation plan: the PDF tree flattened into the canonical form the fused
+// kernel evaluates per event, entirely in registers,
+//
+//     p(x) = sum_i  prod_k  sum_c  coef_{ikc} * leaf_{ikc}(x[col_{ikc}])
+//
+// which covers a single PDF, AddPdf/WeightedSum (nested sums flatten), ProdPdf of
+// 1-D factors (or of sums), AddPdf of ProdPdfs, and the extended AddPdf.  Every
+// normalisation (component norms, fractions / yields, the model norm) is folded
+// into the per-term `coef` on the host, once per parameter point -- the
+// reference's cached constant branch (proj/src/model.cpp:22-28,
+// proj/src/eval.cpp:127-129) -- so the device does no division by N.
+//
+// This header is shared by the host compiler and nvcc.
+#pragma once
+
+#include <cstdint>
+
+namespace ffb {
+
+constexpr int kMaxTerms = 32;
+constexpr int kMaxCols = 8;
+constexpr int kMaxOrder = 12;
+
+enum LeafKind : int {
+  LK_GAUSS = 0,    // c: [coef, mu, -1/(2 sigma^2)]
+  LK_EXPO = 1,     // c: [coef, c]
+  LK_CHISQ = 2,    // c: [coef, k/2 - 1, at_zero]
+  LK_JOHNSON = 3,  // c: [coef, mu, 1/lambda, gamma, delta, delta/(lambda sqrt(2 pi))]
+  LK_ARGUS = 4,    // c: [coef, m0, c, p]
+  LK_CHEB = 5,     // c: [coef, lo+hi, 1/(hi-lo), a1..an]
+  LK_POLY = 6,     // c: [coef, a1..an]
+};
+
+enum TermFlags : int { TF_END_SUM = 1, TF_END_PROD = 2 };
+
+struct DevTerm {
+  int kind;   // LeafKind
+  int col;    // compact column slot (0..ncols-1)
+  int order;  // Chebychev / Polynomial order
+  int flags;  // TermFlags
+  int coff;   // offset of this term's constants in a point's constant row
+};
+
+struct DevPlan {
+  int nterms;
+  int ncols;   // distinct observables read
+  int stride;  // doubles per parameter point
+  int simple;  // 1: a single sum of terms (no product structure)
+  DevTerm t[kMaxTerms];
+};
+
+}  // namespace ffb

@@ -1,0 +1,201 @@
+#include "plan_build.hpp"
+
+#include <cmath>
+
+namespace ffb {
+
+namespace {
+
+constexpr double kSqrt2Pi = 2.5066282746310005024;
+
+// One traversal serves both compile (structure) and build (constants): the
+// flattening depends only on the tree, so every point yields the same terms.
+struct Emitter {
+  const Model& m;
+  const double* theta;  // may be null when only the structure is wanted
+  std::vector<DevTerm> terms;
+  std::vector<double> consts;
+  std::vector<int> col_obs;
+
+  int slot(int obs) {
+    for (std::size_t i = 0; i < col_obs.size(); ++i) {
+      if (col_obs[i] == obs) return static_cast<int>(i);
+    }
+    col_obs.push_back(obs);
+    return static_cast<int>(col_obs.size()) - 1;
+  }
+
+  double norm(int pdf) const { return theta ? m.normalization(pdf, theta) : 1.0; }
+  std::vector<double> fracs(int pdf) const {
+    if (theta) return m.fractions(pdf, theta);
+    return std::vector<double>(m.pdfs[pdf].children.size(), 1.0);
+  }
+  double par(const Pdf& p, int k) const { return theta ? theta[p.params[k]] : 0.0; }
+
+  // scale * unnorm(leaf)
+  void leaf(int id, double scale) {
+    const Pdf& p = m.pdfs[id];
+    DevTerm t{};
+    t.col = slot(p.obs);
+    t.coff = static_cast<int>(consts.size());
+    consts.push_back(scale);
+    switch (p.kind) {
+      case Kind::Gaussian: {  // GaussianKernel, proj/src/pdfs.cpp:15-26
+        t.kind = LK_GAUSS;
+        const double sigma = par(p, 1);
+        consts.push_back(par(p, 0));
+        consts.push_back(theta ? -1.0 / (2.0 * sigma * sigma) : 0.0);
+        break;
+      }
+      case Kind::Exponential:  // ExponentialKernel, proj/src/pdfs.cpp:28-33
+        t.kind = LK_EXPO;
+        consts.push_back(par(p, 0));
+        break;
+      case Kind::ChiSquare: {  // ChiSquareKernel, proj/src/pdfs.cpp:35-52
+        t.kind = LK_CHISQ;
+        const double k = par(p, 0);
+        consts.push_back(0.5 * k - 1.0);
+        consts.push_back(k == 2.0 ? 1.0 : 0.0);
+        break;
+      }
+      case Kind::JohnsonSU: {  // JohnsonKernel, proj/src/pdfs.cpp:54-77
+        t.kind = LK_JOHNSON;
+        const double lambda = theta ? par(p, 1) : 1.0, delta = par(p, 3);
+        consts.push_back(par(p, 0));
+        consts.push_back(1.0 / lambda);
+        consts.push_back(par(p, 2));
+        consts.push_back(delta);
+        consts.push_back(delta / (lambda * kSqrt2Pi));
+        break;
+      }
+      case Kind::ArgusBG:
+        t.kind = LK_ARGUS;
+        consts.push_back(par(p, 0));
+        consts.push_back(par(p, 1));
+        consts.push_back(par(p, 2));
+        break;
+      case Kind::Chebychev: {
+        t.kind = LK_CHEB;
+        t.order = static_cast<int>(p.params.size());
+        const Observable& o = m.observables[p.obs];
+        consts.push_back(o.lo + o.hi);
+        consts.push_back(1.0 / (o.hi - o.lo));
+        for (int k = 0; k < t.order; ++k) consts.push_back(par(p, k));
+        break;
+      }
+      case Kind::Polynomial:
+        t.kind = LK_POLY;
+        t.order = static_cast<int>(p.params.size());
+        for (int k = 0; k < t.order; ++k) consts.push_back(par(p, k));
+        break;
+      default:
+        usage_error("internal: not a leaf");
+    }
+    terms.push_back(t);
+  }
+
+  // scale * unnorm(pdf) for a one-dimensional pdf, as a flat sum of leaves.
+  // WeightedSum: unnorm = sum_i (f_i / N_i) unnorm_i (proj/src/pdfs.cpp:234-257).
+  void sum(int id, double scale) {
+    const Pdf& p = m.pdfs[id];
+    if (is_leaf(p.kind)) {
+      leaf(id, scale);
+    } else if (p.kind == Kind::ProdPdf && p.children.size() == 1) {
+      sum(p.children[0], scale);
+    } else if ((p.kind == Kind::WeightedSum || p.kind == Kind::AddExtended) && p.obs >= 0) {
+      const std::vector<double> f = fracs(id);
+      for (std::size_t i = 0; i < p.children.size(); ++i) {
+        const double coef = theta ? f[i] / norm(p.children[i]) : 1.0;
+        sum(p.children[i], scale * coef);
+      }
+    } else {
+      usage_error("pdf '" + p.name + "' (" + kind_name(p.kind) +
+                  ") nests a product inside a one-dimensional sum; the GPU plan supports "
+                  "sum-of-products-of-sums trees");
+    }
+  }
+
+  void end(int flags) { terms.back().flags |= flags; }
+
+  void factors(int id, std::vector<int>& out) {
+    const Pdf& p = m.pdfs[id];
+    if (p.kind == Kind::ProdPdf) {
+      for (const int c : p.children) factors(c, out);
+    } else {
+      out.push_back(id);
+    }
+  }
+
+  // scale * unnorm(ProdPdf) = scale * prod_k unnorm_k (restated ProdPdf).
+  void product(int id, double scale) {
+    std::vector<int> fs;
+    factors(id, fs);
+    for (std::size_t k = 0; k < fs.size(); ++k) {
+      sum(fs[k], k == 0 ? scale : 1.0);
+      end(TF_END_SUM);
+    }
+  }
+
+  void root(int id, double scale) {
+    const Pdf& p = m.pdfs[id];
+    if (p.kind == Kind::ProdPdf) {
+      product(id, scale);
+      end(TF_END_PROD);
+    } else if (p.obs >= 0) {
+      sum(id, scale);
+      end(TF_END_SUM | TF_END_PROD);
+    } else {  // sum over products on several observables
+      const std::vector<double> f = fracs(id);
+      for (std::size_t i = 0; i < p.children.size(); ++i) {
+        const int c = p.children[i];
+        const double coef = theta ? f[i] / norm(c) : 1.0;
+        if (m.pdfs[c].kind == Kind::ProdPdf) {
+          product(c, scale * coef);
+        } else {
+          sum(c, scale * coef);
+          end(TF_END_SUM);
+        }
+        end(TF_END_PROD);
+      }
+    }
+  }
+};
+
+}  // namespace
+
+HostPlan compile_plan(const Model& m, int pdf, bool normalized) {
+  Emitter e{m, nullptr, {}, {}, {}};
+  e.root(pdf, 1.0);
+  if (e.terms.size() > static_cast<std::size_t>(kMaxTerms)) {
+    usage_error("model has " + std::to_string(e.terms.size()) + " leaf terms; the GPU plan holds " +
+                std::to_string(kMaxTerms));
+  }
+  if (e.col_obs.size() > static_cast<std::size_t>(kMaxCols)) {
+    usage_error("model reads more than " + std::to_string(kMaxCols) + " observables");
+  }
+  HostPlan hp;
+  hp.pdf = pdf;
+  hp.normalized = normalized;
+  hp.col_obs = e.col_obs;
+  hp.dev.nterms = static_cast<int>(e.terms.size());
+  hp.dev.ncols = static_cast<int>(e.col_obs.size());
+  hp.dev.stride = static_cast<int>(e.consts.size());
+  int ends = 0;
+  for (std::size_t i = 0; i < e.terms.size(); ++i) {
+    hp.dev.t[i] = e.terms[i];
+    if (e.terms[i].flags) ++ends;
+  }
+  hp.dev.simple = ends == 1 ? 1 : 0;
+  return hp;
+}
+
+void build_constants(const HostPlan& plan, const Model& m, const double* theta, double* row) {
+  m.check_params(plan.pdf, theta);
+  const double scale = plan.normalized ? 1.0 / m.normalization(plan.pdf, theta) : 1.0;
+  Emitter e{m, theta, {}, {}, {}};
+  e.root(plan.pdf, scale);
+  if (static_cast<int>(e.consts.size()) != plan.dev.stride) usage_error("internal: plan drift");
+  for (int i = 0; i < plan.dev.stride; ++i) row[i] = e.consts[i];
+}
+
+}  // namespace ffb

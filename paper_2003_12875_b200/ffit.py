@@ -1,0 +1,405 @@
+"""Python mirror of the reference's likelihood interface, over the C ABI.
+
+Names follow the reference (proj/include/ffit/eval.hpp:12-44, model.hpp, fit.hpp,
+include/ffit.h): ``Model.from_string``, ``DataSet``, ``nll(model, ds, mode)`` ->
+``NllValue``, ``probabilities``, ``normalization``, ``fit_to`` -> ``FitResult``,
+with the GPU extensions (``nll_points``, ``eval_batch``, ``fit_gradient``,
+device-resident datasets).  Errors raise ``FfitError`` carrying the reference's
+status codes (1 usage, 2 data, 3 numeric; proj/include/ffit/errors.hpp:9-24).
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ._lib import CP, DP, LL, ULL, VP, lib
+
+
+class FfitError(RuntimeError):
+    def __init__(self, code, message):
+        super().__init__(f"[{code}] {message}")
+        self.code = code
+        self.message = message
+
+
+USAGE, DATA, NUMERIC = 1, 2, 3
+NO_INVALID = 0xFFFFFFFFFFFFFFFF
+
+
+class EvalMode(enum.IntEnum):
+    Scalar = 0
+    BatchPrecise = 1
+    BatchFast = 2
+    Gpu = 3
+
+
+def _check(rc):
+    if rc:
+        raise FfitError(rc, lib().ffit_last_error().decode())
+
+
+def _dp(a):
+    return a.ctypes.data_as(DP)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+class Model:
+    """A parsed model (observables, parameters, PDF tree) with its GPU engine."""
+
+    def __init__(self, handle, text=None):
+        self._h = handle
+        self.text = text
+
+    @classmethod
+    def from_string(cls, text: str) -> "Model":
+        h = VP()
+        _check(lib().ffit_model_parse(text.encode(), ctypes.byref(h)))
+        return cls(h, text)
+
+    @classmethod
+    def from_file(cls, path: str) -> "Model":
+        h = VP()
+        _check(lib().ffit_model_load(path.encode(), ctypes.byref(h)))
+        with open(path) as fh:
+            return cls(h, fh.read())
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and lib is not None:
+            lib().ffit_model_free(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def param_names(self):
+        L = lib()
+        return [L.ffit_model_param_name(self._h, i).decode() for i in range(L.ffit_model_param_count(self._h))]
+
+    @property
+    def observables(self):
+        L = lib()
+        return [L.ffcu_model_observable_name(self._h, i).decode()
+                for i in range(L.ffcu_model_observable_count(self._h))]
+
+    @property
+    def pdf_names(self):
+        L = lib()
+        return [L.ffcu_model_pdf_name(self._h, i).decode() for i in range(L.ffcu_model_pdf_count(self._h))]
+
+    def observable_range(self):
+        lo, hi = ctypes.c_double(), ctypes.c_double()
+        _check(lib().ffit_model_observable_range(self._h, ctypes.byref(lo), ctypes.byref(hi)))
+        return lo.value, hi.value
+
+    def set(self, name, value):
+        _check(lib().ffit_model_set_param(self._h, name.encode(), float(value)))
+
+    def get(self, name):
+        v, e = ctypes.c_double(), ctypes.c_double()
+        _check(lib().ffit_model_get_param(self._h, name.encode(), ctypes.byref(v), ctypes.byref(e)))
+        return v.value, e.value
+
+    def is_constant(self, name):
+        c = ctypes.c_int()
+        _check(lib().ffit_model_param_is_constant(self._h, name.encode(), ctypes.byref(c)))
+        return bool(c.value)
+
+    def theta(self):
+        return np.array([self.get(n)[0] for n in self.param_names])
+
+    def plan(self):
+        """The flattened evaluation plan: (terms, ncols, stride)."""
+        L = lib()
+        nt, nc, st = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        _check(L.ffcu_plan_info(self._h, ctypes.byref(nt), ctypes.byref(nc), ctypes.byref(st)))
+        terms = []
+        for i in range(nt.value):
+            vals = [ctypes.c_int() for _ in range(5)]
+            _check(L.ffcu_plan_term(self._h, i, *[ctypes.byref(v) for v in vals]))
+            terms.append(dict(zip(("kind", "col", "order", "flags", "coff"), [v.value for v in vals])))
+        return terms, nc.value, st.value
+
+    def point_constants(self, point=None):
+        _, _, stride = self.plan()
+        row = np.empty(stride)
+        p = None if point is None else _f64(point)
+        _check(lib().ffcu_point_constants(self._h, None if p is None else _dp(p), _dp(row)))
+        return row
+
+    def extended_terms(self, points, n_events):
+        pts = _f64(np.atleast_2d(points))
+        out = np.empty(pts.shape[0])
+        _check(lib().ffcu_extended_terms(self._h, _dp(pts), pts.shape[0], float(n_events), _dp(out)))
+        return out
+
+
+class DataSet:
+    """SoA fp64 event columns resident in HBM (reference DataSet, dataset.hpp:20-51)."""
+
+    def __init__(self, handle, keep=None):
+        self._h = handle
+        self._keep = keep  # objects whose memory a view aliases
+
+    @classmethod
+    def from_columns(cls, columns: dict) -> "DataSet":
+        names = list(columns)
+        cols = [_f64(columns[n]) for n in names]
+        n = len(cols[0]) if cols else 0
+        if any(len(c) != n for c in cols):
+            raise FfitError(USAGE, "columns have unequal lengths")
+        cn = (CP * len(names))(*[s.encode() for s in names])
+        cp = (DP * len(cols))(*[_dp(c) for c in cols])
+        h = VP()
+        _check(lib().ffcu_dataset_from_host(cn, cp, len(names), n, ctypes.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def from_device(cls, columns: dict, device: int = 0) -> "DataSet":
+        """Zero-copy view over device tensors (anything with data_ptr())."""
+        names = list(columns)
+        tensors = [columns[n] for n in names]
+        n = int(tensors[0].numel()) if tensors else 0
+        cn = (CP * len(names))(*[s.encode() for s in names])
+        cp = (VP * len(names))(*[t.data_ptr() for t in tensors])
+        h = VP()
+        _check(lib().ffcu_dataset_from_device(cn, cp, len(names), n, device, ctypes.byref(h)))
+        return cls(h, keep=tensors)
+
+    @classmethod
+    def sample(cls, model: Model, n: int, seed: int):
+        h = VP()
+        eff = ctypes.c_double()
+        _check(lib().ffit_sample(model.handle, n, seed, ctypes.byref(h), ctypes.byref(eff)))
+        return cls(h), eff.value
+
+    @classmethod
+    def read_csv(cls, model: Model, path: str):
+        h = VP()
+        dropped = ctypes.c_long()
+        _check(lib().ffit_dataset_read_csv(model.handle, path.encode(), ctypes.byref(h), ctypes.byref(dropped)))
+        return cls(h), dropped.value
+
+    def write_csv(self, path):
+        _check(lib().ffit_dataset_write_csv(self._h, path.encode()))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and lib is not None:
+            lib().ffit_dataset_free(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def n_rows(self):
+        return int(lib().ffit_dataset_rows(self._h))
+
+    def __len__(self):
+        return self.n_rows
+
+    @property
+    def names(self):
+        L = lib()
+        return [L.ffcu_dataset_column_name(self._h, i).decode() for i in range(L.ffcu_dataset_ncols(self._h))]
+
+    def column(self, name) -> np.ndarray:
+        out = np.empty(self.n_rows)
+        _check(lib().ffcu_dataset_download(self._h, self.names.index(name), _dp(out)))
+        return out
+
+    def copy_from_host(self, columns: dict):
+        cols = [_f64(columns[n]) for n in self.names]
+        cp = (DP * len(cols))(*[_dp(c) for c in cols])
+        _check(lib().ffcu_dataset_copy_from_host(self._h, cp))
+
+    def slice(self, begin, end) -> "DataSet":
+        h = VP()
+        _check(lib().ffcu_dataset_slice(self._h, begin, end, ctypes.byref(h)))
+        return DataSet(h, keep=self)
+
+
+@dataclass
+class NllValue:
+    """proj/include/ffit/eval.hpp:14-21"""
+    value: float = 0.0
+    n_entries: int = 0
+    n_evaluations: int = 0
+    first_invalid: int = -1
+
+
+def nll(model: Model, ds: DataSet, mode: EvalMode = EvalMode.Gpu) -> NllValue:
+    """Reference ffit::nll (proj/src/eval.cpp:165-172) on the GPU.
+
+    first_invalid comes from the multi-point entry (same launch)."""
+    v = ctypes.c_double()
+    ne = ctypes.c_ulonglong()
+    if int(mode) == EvalMode.Scalar:
+        _check(lib().ffit_nll(model.handle, ds.handle, int(mode), ctypes.byref(v), ctypes.byref(ne)))
+    vals, bad, launches = nll_points(model, ds, model.theta()[None, :])
+    return NllValue(float(vals[0]), ds.n_rows, int(launches), int(bad[0]))
+
+
+def nll_c(model: Model, ds: DataSet, mode: EvalMode = EvalMode.Gpu):
+    """ffit_nll exactly as the reference C ABI exposes it: (value, n_evaluations)."""
+    v = ctypes.c_double()
+    ne = ctypes.c_ulonglong()
+    _check(lib().ffit_nll(model.handle, ds.handle, int(mode), ctypes.byref(v), ctypes.byref(ne)))
+    return v.value, ne.value
+
+
+def nll_points(model: Model, ds: DataSet, points):
+    """NLL at P parameter points (rows over model.param_names) in one launch.
+    Returns (values[P], first_invalid[P], kernel launches)."""
+    pts = _f64(np.atleast_2d(points))
+    P = pts.shape[0]
+    vals = np.empty(P)
+    bad = np.empty(P, dtype=np.int64)
+    ne = ctypes.c_ulonglong()
+    _check(lib().ffcu_nll_points(model.handle, ds.handle, _dp(pts), P, _dp(vals),
+                                 bad.ctypes.data_as(ctypes.POINTER(LL)), ctypes.byref(ne)))
+    return vals, bad, ne.value
+
+
+def nll_points_partial(model: Model, ds: DataSet, points):
+    """Uncombined Neumaier pairs (P x 2) of the event sum, for cross-rank combining."""
+    pts = _f64(np.atleast_2d(points))
+    P = pts.shape[0]
+    sc = np.empty((P, 2))
+    bad = np.empty(P, dtype=np.int64)
+    _check(lib().ffcu_nll_points_partial(model.handle, ds.handle, _dp(pts), P, _dp(sc),
+                                         bad.ctypes.data_as(ctypes.POINTER(LL)), None))
+    return sc, bad
+
+
+def nll_points_device(model: Model, ds: DataSet, points, d_sc_ptr, d_bad_ptr, stream_ptr=None):
+    """Async multi-point NLL into device buffers (2P doubles, P uint64) on a CUDA stream."""
+    pts = _f64(np.atleast_2d(points))
+    ne = ctypes.c_ulonglong()
+    _check(lib().ffcu_nll_points_device(model.handle, ds.handle, _dp(pts), pts.shape[0],
+                                        VP(d_sc_ptr), VP(d_bad_ptr), VP(stream_ptr or 0),
+                                        ctypes.byref(ne)))
+    return ne.value
+
+
+def combine_pairs_device(d_in_ptr, R, P, d_out_ptr, stream_ptr=None):
+    _check(lib().ffcu_combine_pairs_device(VP(d_in_ptr), R, P, VP(d_out_ptr), VP(stream_ptr or 0)))
+
+
+def probabilities(model: Model, ds: DataSet, mode: EvalMode = EvalMode.Gpu, point=None) -> np.ndarray:
+    """Reference ffit::probabilities (proj/src/eval.cpp:174-192) on the GPU."""
+    out = np.empty(ds.n_rows)
+    if point is None:
+        _check(lib().ffit_probabilities(model.handle, ds.handle, int(mode), _dp(out)))
+    else:
+        p = _f64(point)
+        _check(lib().ffcu_probabilities_at(model.handle, ds.handle, _dp(p), _dp(out)))
+    return out
+
+
+def eval_batch(model: Model, pdf: str, ds: DataSet) -> np.ndarray:
+    """PdfSpec::eval_batch (proj/src/pdfs.cpp:212-269): unnormalised values of a named pdf."""
+    out = np.empty(ds.n_rows)
+    _check(lib().ffcu_eval_batch(model.handle, pdf.encode(), ds.handle, _dp(out)))
+    return out
+
+
+def normalization(model: Model, pdf: str | None = None, point=None) -> float:
+    out = ctypes.c_double()
+    p = None if point is None else _f64(point)
+    _check(lib().ffcu_normalization(model.handle, None if pdf is None else pdf.encode(),
+                                    None if p is None else _dp(p), ctypes.byref(out)))
+    return out.value
+
+
+@dataclass
+class FittedParameter:
+    name: str
+    value: float
+    uncertainty: float
+
+
+@dataclass
+class FitResult:
+    """proj/include/ffit/fit.hpp:25-33"""
+    converged: bool
+    nll_min: float
+    parameters: list
+    n_nll_calls: int
+    wall_seconds: float
+    uncertainties_valid: bool
+    iterations: int = 0
+    n_launches: int = 0
+    trace: list = field(default_factory=list)
+
+    def value(self, name):
+        return next(p.value for p in self.parameters if p.name == name)
+
+
+def _result(h) -> FitResult:
+    L = lib()
+    try:
+        params = [FittedParameter(L.ffit_result_param_name(h, i).decode(), L.ffit_result_param_value(h, i),
+                                  L.ffit_result_param_uncertainty(h, i))
+                  for i in range(L.ffit_result_param_count(h))]
+        n = L.ffcu_result_trace(h, None, 0)
+        tr = np.empty(max(n, 1))
+        L.ffcu_result_trace(h, _dp(tr), n)
+        return FitResult(bool(L.ffit_result_converged(h)), L.ffit_result_nll(h), params,
+                         int(L.ffit_result_nll_calls(h)), L.ffit_result_wall_seconds(h),
+                         bool(L.ffit_result_uncertainties_valid(h)), L.ffcu_result_iterations(h),
+                         int(L.ffcu_result_launches(h)), list(tr[:n]))
+    finally:
+        L.ffit_result_free(h)
+
+
+def fit_to(model: Model, ds: DataSet, mode: EvalMode = EvalMode.Gpu, tolerance=0.0, max_iterations=0) -> FitResult:
+    """Reference fit_to (proj/src/fit.cpp:86-251): Nelder-Mead, batched GPU points."""
+    h = VP()
+    _check(lib().ffit_fit(model.handle, ds.handle, int(mode), tolerance, max_iterations, ctypes.byref(h)))
+    return _result(h)
+
+
+def fit_gradient(model: Model, ds: DataSet, tolerance=0.0, max_iterations=0) -> FitResult:
+    """Minuit-style BFGS on central differences: 2d+1 points per launch."""
+    h = VP()
+    _check(lib().ffcu_fit_gradient(model.handle, ds.handle, tolerance, max_iterations, ctypes.byref(h)))
+    return _result(h)
+
+
+def last_launch(model: Model) -> dict:
+    info = (ctypes.c_int * 6)()
+    _check(lib().ffcu_last_launch(model.handle, info))
+    return dict(zip(("threads", "events_per_thread", "tile", "ntiles", "nchunks", "grid"), list(info)))
+
+
+def kernel_launches() -> int:
+    return int(lib().ffcu_kernel_launches())
+
+
+def fp64_peak():
+    """Measured FP64 FMA instructions/s on the current device (and the ms it took)."""
+    v = ctypes.c_double()
+    ms = ctypes.c_float()
+    _check(lib().ffcu_fp64_peak(ctypes.byref(v), ctypes.byref(ms)))
+    return v.value, ms.value
+
+
+def sample_host(model: Model, n: int, seed: int):
+    """Seeded generator into host arrays, one per observable (name -> array)."""
+    names = model.observables
+    cols = [np.empty(n) for _ in names]
+    cp = (DP * len(cols))(*[_dp(c) for c in cols])
+    eff = ctypes.c_double()
+    _check(lib().ffcu_sample_host(model.handle, n, seed, cp, ctypes.byref(eff)))
+    return dict(zip(names, cols)), eff.value

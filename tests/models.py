@@ -1,0 +1,159 @@
+"""Model texts shared by the tests and the golden-fixture generator.
+
+REF_MODELS use only the reference grammar (proj/docs/model-file.md), so the very same
+text runs through the reference engine, the oracle and the GPU product.  The first five
+are the acceptance-suite models (proj/tests/acceptance.cpp:38-80); `gauss_c1` is the
+BASELINE config-1 shape.
+
+EXPR_MODELS pair a restated kind (ArgusBG, Chebychev, Polynomial) with the reference's
+Expression spelling of the same density.
+"""
+
+MIX = """
+observable x -5 5
+parameter mu 0.2 -2 2
+parameter sigma 0.8 0.1 3
+parameter c -0.35 -3 0
+parameter f 0.4 0.05 0.95
+pdf s Gaussian(x, mu, sigma)
+pdf b Exponential(x, c)
+pdf m WeightedSum(s, f, b)
+"""
+
+REF_MODELS = {
+    "gauss": ("""
+observable x -5 5
+parameter mu 0.3 -2 2
+parameter sigma 1.1 0.1 3
+pdf g Gaussian(x, mu, sigma)
+""", 8675309),
+    "expo": ("""
+observable x 0 8
+parameter c -0.6 -3 0
+pdf e Exponential(x, c)
+""", 8675309),
+    "chisq": ("""
+observable x 0.1 15
+parameter k 3.5 0.5 20
+pdf q ChiSquare(x, k)
+""", 8675309),
+    "johnson": ("""
+observable x -6 6
+parameter mu 0.1 -2 2
+parameter lambda 1.2 0.1 3
+parameter gamma -0.3 -3 3
+parameter delta 1.4 0.1 3
+pdf j JohnsonSU(x, mu, lambda, gamma, delta)
+""", 8675309),
+    "mix": (MIX, 8675309),
+    "gauss_c1": ("""
+observable x -10 10
+parameter mean 1.0 -5 5
+parameter sigma 2.0 0.1 10
+pdf g Gaussian(x, mean, sigma)
+""", 1001),
+    "mix3_nested": ("""
+observable x -6 6
+parameter m1 -2 -5 5
+parameter s1 0.5 0.1 3
+parameter m2 1.5 -5 5
+parameter s2 0.9 0.1 3
+parameter c -0.3 -3 3
+parameter f1 0.3 0 1
+parameter f2 0.25 0 1
+parameter g 0.6 0 1
+pdf a Gaussian(x, m1, s1)
+pdf b Gaussian(x, m2, s2)
+pdf e Exponential(x, c)
+pdf ab WeightedSum(a, g, b)
+pdf m WeightedSum(ab, f1, e, f2, a)
+""", 77),
+    "mix_chisq": ("""
+observable x 0.1 12
+parameter k 4.5 0.5 20
+parameter mu 6 0 12
+parameter sigma 1.0 0.1 3
+parameter f 0.7 0 1
+pdf q ChiSquare(x, k)
+pdf g Gaussian(x, mu, sigma)
+pdf m WeightedSum(q, f, g)
+""", 5),
+}
+
+ARGUS_REF = """
+observable x 5.2 5.29
+parameter m 5.279 5.2 5.29
+parameter s 0.003 0.001 0.01
+parameter m0 5.291 5.0 5.4 const
+parameter c -20 -100 10
+parameter f 0.1 0 1
+pdf sig Gaussian(x, m, s)
+pdf bkg Expression("x*sqrt(1-(x/m0)^2)*exp(c*(1-(x/m0)^2))", x, m0, c)
+pdf model WeightedSum(sig, f, bkg)
+"""
+
+ARGUS_OURS = """
+observable x 5.2 5.29
+parameter m 5.279 5.2 5.29
+parameter s 0.003 0.001 0.01
+parameter m0 5.291 5.0 5.4 const
+parameter c -20 -100 10
+parameter p 0.5 0 1 const
+parameter f 0.1 0 1
+pdf sig Gaussian(x, m, s)
+pdf bkg ArgusBG(x, m0, c, p)
+pdf model WeightedSum(sig, f, bkg)
+"""
+
+EXPR_MODELS = {
+    "argus_mix": (ARGUS_REF, ARGUS_OURS, 1002, "x"),
+    "argus_only": ("""
+observable x 5.2 5.29
+parameter m0 5.291 5.0 5.4 const
+parameter c -20 -100 10
+pdf bkg Expression("x*sqrt(1-(x/m0)^2)*exp(c*(1-(x/m0)^2))", x, m0, c)
+""", """
+observable x 5.2 5.29
+parameter m0 5.291 5.0 5.4 const
+parameter c -20 -100 10
+parameter p 0.5 0 1 const
+pdf bkg ArgusBG(x, m0, c, p)
+""", 11, "x"),
+    "cheb3": ("""
+observable z -1 1
+parameter a1 0.2 -1 1
+parameter a2 -0.1 -1 1
+parameter a3 0.05 -1 1
+pdf ch Expression("1 + a1*z + a2*(2*z^2-1) + a3*(4*z^3-3*z)", z, a1, a2, a3)
+""", """
+observable z -1 1
+parameter a1 0.2 -1 1
+parameter a2 -0.1 -1 1
+parameter a3 0.05 -1 1
+pdf ch Chebychev(z, a1, a2, a3)
+""", 1023, "z"),
+    "cheb3_shifted": ("""
+observable z 2 6
+parameter a1 0.3 -1 1
+parameter a2 0.1 -1 1
+parameter a3 -0.05 -1 1
+pdf ch Expression("1 + a1*((2*z-8)/4) + a2*(2*((2*z-8)/4)^2-1) + a3*(4*((2*z-8)/4)^3-3*((2*z-8)/4))", z, a1, a2, a3)
+""", """
+observable z 2 6
+parameter a1 0.3 -1 1
+parameter a2 0.1 -1 1
+parameter a3 -0.05 -1 1
+pdf ch Chebychev(z, a1, a2, a3)
+""", 31, "z"),
+    "poly2": ("""
+observable x -1 2
+parameter a1 0.2 -1 1
+parameter a2 0.1 -1 1
+pdf po Expression("1 + a1*x + a2*x^2", x, a1, a2)
+""", """
+observable x -1 2
+parameter a1 0.2 -1 1
+parameter a2 0.1 -1 1
+pdf po Polynomial(x, a1, a2)
+""", 13, "x"),
+}
