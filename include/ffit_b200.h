@@ -178,6 +178,11 @@ int ffcu_result_trace(const ffit_fit_result* r, double* out, int cap);
 
 /* Last fused-NLL launch shape: threads, events/thread, tile, tiles, chunks, grid. */
 int ffcu_last_launch(const ffit_model* m, int* info6);
+/* CUDA-event timing of every fused NLL kernel launch while enabled (on the
+ * launching stream); _read synchronises, returns the summed ms and the launch
+ * count, and clears. */
+int ffcu_kernel_timer(int enable);
+int ffcu_kernel_timer_read(double* total_ms, unsigned long long* count);
 /* Kernels this library has launched in this process. */
 unsigned long long ffcu_kernel_launches(void);
 /* Measured FP64 FMA instructions per second on the current device. */

@@ -85,6 +85,8 @@ SIGNATURES = {
     "ffcu_result_trace": (I, [VP, DP, I]),
     "ffcu_last_launch": (I, [VP, IP]),
     "ffcu_kernel_launches": (ULL, []),
+    "ffcu_kernel_timer": (I, [I]),
+    "ffcu_kernel_timer_read": (I, [DP, ULLP]),
     "ffcu_fp64_peak": (I, [DP, ctypes.POINTER(ctypes.c_float)]),
     "ffcu_sample_host": (I, [VP, LL, ULL, ctypes.POINTER(DP), DP]),
 }

@@ -690,6 +690,17 @@ FFB_API int ffcu_last_launch(const ffit_model* m, int* info6) {
 
 FFB_API unsigned long long ffcu_kernel_launches(void) { return ffb::kernel_launches(); }
 
+FFB_API int ffcu_kernel_timer(int enable) {
+  return guarded([&] { ffb::kernel_timer_enable(enable != 0); });
+}
+
+FFB_API int ffcu_kernel_timer_read(double* total_ms, unsigned long long* count) {
+  return guarded([&] {
+    require(total_ms, "total_ms");
+    *total_ms = ffb::kernel_timer_read(count);
+  });
+}
+
 FFB_API int ffcu_fp64_peak(double* fma_per_s, float* ms) {
   return guarded([&] {
     require(fma_per_s, "fma_per_s");

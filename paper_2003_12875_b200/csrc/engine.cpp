@@ -4,6 +4,8 @@
 #include <cmath>
 #include <cstring>
 #include <limits>
+#include <mutex>
+#include <utility>
 
 namespace ffb {
 
@@ -13,6 +15,33 @@ std::atomic<unsigned long long> g_launches{0};
 constexpr int kMaxPointsPerLaunch = 512;
 
 }  // namespace
+
+namespace {
+std::mutex g_timer_mu;
+bool g_timer_on = false;
+std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_timer_events;
+}  // namespace
+
+void kernel_timer_enable(bool on) {
+  std::lock_guard<std::mutex> lk(g_timer_mu);
+  g_timer_on = on;
+}
+
+double kernel_timer_read(unsigned long long* count) {
+  std::lock_guard<std::mutex> lk(g_timer_mu);
+  double total = 0.0;
+  for (auto& [a, b] : g_timer_events) {
+    cuda_check(cudaEventSynchronize(b), "cudaEventSynchronize(timer)");
+    float ms = 0.f;
+    cuda_check(cudaEventElapsedTime(&ms, a, b), "cudaEventElapsedTime");
+    total += ms;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+  if (count) *count = g_timer_events.size();
+  g_timer_events.clear();
+  return total;
+}
 
 unsigned long long kernel_launches() { return g_launches.load(); }
 void count_launches(unsigned long long k) { g_launches += k; }
@@ -242,7 +271,16 @@ int Engine::nll_points_device(const DeviceDataset& ds, const double* thetas, int
   } else {
     ColPtrs cols;
     bind_columns(plan_, ds, cols);
-    last_ = launch_nll(plan_.dev, cols, ds.n, d_consts, P, d_scratch_, d_pairs, d_bad, s);
+    cudaEvent_t ea = nullptr, eb = nullptr;
+    {
+      std::lock_guard<std::mutex> lk(g_timer_mu);
+      if (g_timer_on) {
+        cuda_check(cudaEventCreate(&ea), "cudaEventCreate");
+        cuda_check(cudaEventCreate(&eb), "cudaEventCreate");
+        g_timer_events.emplace_back(ea, eb);
+      }
+    }
+    last_ = launch_nll(plan_.dev, cols, ds.n, d_consts, P, d_scratch_, d_pairs, d_bad, s, ea, eb);
     launches = last_.launches;
     cuda_check(cudaGetLastError(), "launch_nll");
   }

@@ -117,6 +117,12 @@ class Engine {
   NllLaunchInfo last_{};
 };
 
+// Optional per-launch timing of the fused NLL kernel (CUDA events on the
+// launching stream), for the live roofline in bench.py.
+void kernel_timer_enable(bool on);
+// Synchronises on the recorded events; returns summed ms and count, then clears.
+double kernel_timer_read(unsigned long long* count);
+
 // Process-wide count of kernels this library launched.
 unsigned long long kernel_launches();
 void count_launches(unsigned long long k);

@@ -41,9 +41,11 @@ std::size_t nll_scratch_bytes(long long n, int P, int ncols);
 //   partials, then a deterministic fixed-order pass over the partials.
 // out[p] = (s, c) with NLL_events(p) = s + c; bad[p] = smallest event index with
 // p <= 0 or non-finite (kNoInvalid if none).  `scratch` holds nll_scratch_bytes.
+// ev_start / ev_stop (may be null) are recorded around the fused kernel alone.
 NllLaunchInfo launch_nll(const DevPlan& plan, const ColPtrs& cols, long long n,
                          const double* d_consts, int P, void* scratch, SumPair* d_out,
-                         unsigned long long* d_bad, cudaStream_t stream);
+                         unsigned long long* d_bad, cudaStream_t stream,
+                         cudaEvent_t ev_start = nullptr, cudaEvent_t ev_stop = nullptr);
 
 // Per-event values of the plan for one point (probabilities() when the plan is
 // normalised, PdfSpec::eval_batch when not).

@@ -383,6 +383,18 @@ def last_launch(model: Model) -> dict:
     return dict(zip(("threads", "events_per_thread", "tile", "ntiles", "nchunks", "grid"), list(info)))
 
 
+def kernel_timer(enable: bool):
+    _check(lib().ffcu_kernel_timer(1 if enable else 0))
+
+
+def kernel_timer_read():
+    """(summed ms, launches) of the fused NLL kernel since the last read."""
+    ms = ctypes.c_double()
+    cnt = ctypes.c_ulonglong()
+    _check(lib().ffcu_kernel_timer_read(ctypes.byref(ms), ctypes.byref(cnt)))
+    return ms.value, cnt.value
+
+
 def kernel_launches() -> int:
     return int(lib().ffcu_kernel_launches())
 
