@@ -106,6 +106,8 @@ void orc_rng_gauss(unsigned long long seed, long long n, double* out) {
   for (long long i = 0; i < n; ++i) out[i] = rng_gauss(&r);
 }
 
+static int contains_prod(const orc_node* nodes, int id);
+
 /* ------------------------------------------------------------------------ */
 /* kernels                                                                   */
 
@@ -309,8 +311,9 @@ static int analytic(const orc_node* nodes, int id, const double* theta, double l
         *out = 0.0;
         return 1;
       }
-      const double ra = a / m0, rb = b / m0;
-      const double ta = 1.0 - ra * ra, tb = 1.0 - rb * rb;
+      /* t = 1 - (x/m0)^2 = (m0-x)(m0+x)/m0^2, written without the cancellation */
+      const double ta = ((m0 - a) * (m0 + a)) / (m0 * m0);
+      const double tb = ((m0 - b) * (m0 + b)) / (m0 * m0);
       *out = 0.5 * m0 * m0 * (argus_G(c, ta) - argus_G(c, tb));
       return 1;
     }
@@ -335,6 +338,16 @@ static int analytic(const orc_node* nodes, int id, const double* theta, double l
       *out = s;
       return 1;
     }
+    case ORC_PROD: { /* restated ProdPdf: product of the factor normalisations */
+      double r = 1.0;
+      for (int i = 0; i < nd->nchild; ++i) {
+        double ni;
+        if (orc_normalization(nodes, nd->child[i], theta, &ni)) return 0;
+        r *= ni;
+      }
+      *out = r;
+      return 1;
+    }
     case ORC_WSUM:
     case ORC_ADDEXT: { /* proj/src/pdfs.cpp:288-300: sum f_i * part_i / norm_i */
       double f[ORC_MAXC + 1];
@@ -342,8 +355,9 @@ static int analytic(const orc_node* nodes, int id, const double* theta, double l
       double acc = 0.0;
       for (int i = 0; i < nd->nchild; ++i) {
         double part, norm;
+        const orc_node* ch = &nodes[nd->child[i]];
         if (!analytic(nodes, nd->child[i], theta, lo, hi, &part)) return 0;
-        analytic(nodes, nd->child[i], theta, nd->lo, nd->hi, &norm);
+        analytic(nodes, nd->child[i], theta, ch->lo, ch->hi, &norm);
         acc += f[i] * part / norm;
       }
       *out = acc;
@@ -364,6 +378,10 @@ int orc_simpson_norm(const orc_node* nodes, int id, const double* theta, double*
 int orc_normalization(const orc_node* nodes, int id, const double* theta, double* out) {
   const orc_node* nd = &nodes[id];
   double r;
+  int multi = 0; /* a sum over products on several observables */
+  if (nd->kind == ORC_WSUM || nd->kind == ORC_ADDEXT) {
+    for (int i = 0; i < nd->nchild; ++i) multi |= contains_prod(nodes, nd->child[i]);
+  }
   if (nd->kind == ORC_PROD) {
     r = 1.0;
     for (int i = 0; i < nd->nchild; ++i) {
@@ -371,6 +389,16 @@ int orc_normalization(const orc_node* nodes, int id, const double* theta, double
       const int rc = orc_normalization(nodes, nd->child[i], theta, &ni);
       if (rc) return rc;
       r *= ni;
+    }
+  } else if (multi) { /* sum_i f_i N_i / N_i */
+    double f[ORC_MAXC + 1];
+    fractions(nd, theta, f);
+    r = 0.0;
+    for (int i = 0; i < nd->nchild; ++i) {
+      double ni;
+      const int rc = orc_normalization(nodes, nd->child[i], theta, &ni);
+      if (rc) return rc;
+      r += f[i] * ni / ni;
     }
   } else if (!analytic(nodes, id, theta, nd->lo, nd->hi, &r)) {
     const int rc = orc_simpson_norm(nodes, id, theta, &r);
@@ -751,9 +779,17 @@ static void prepare_bounds(sampler* s, int id) {
   for (int i = 0; i < nd->nchild; ++i) prepare_bounds(s, nd->child[i]);
 }
 
+static int contains_prod(const orc_node* nodes, int id) {
+  if (nodes[id].kind == ORC_PROD) return 1;
+  for (int i = 0; i < nodes[id].nchild; ++i)
+    if (contains_prod(nodes, nodes[id].child[i])) return 1;
+  return 0;
+}
+
 static int sample_1d(const orc_node* nodes, int id, const double* theta, long long n,
                      unsigned long long seed, double* out, unsigned long long* proposed,
                      unsigned long long* accepted) {
+  if (contains_prod(nodes, id)) return fail(1, "sampling needs a one-dimensional pdf per factor");
   sampler* s = (sampler*)calloc(1, sizeof(sampler));
   s->nodes = nodes;
   s->theta = theta;

@@ -429,8 +429,9 @@ std::optional<double> Model::analytic_integral(int id, double lo, double hi,
       const double a = lo > 0.0 ? lo : 0.0;
       const double b = hi < m0 ? hi : m0;
       if (!(a < b)) return 0.0;
-      const double ra = a / m0, rb = b / m0;
-      const double ta = 1.0 - ra * ra, tb = 1.0 - rb * rb;
+      // t = 1 - (x/m0)^2 = (m0-x)(m0+x)/m0^2, written without the cancellation
+      const double ta = ((m0 - a) * (m0 + a)) / (m0 * m0);
+      const double tb = ((m0 - b) * (m0 + b)) / (m0 * m0);
       return 0.5 * m0 * m0 * (argus_G(c, ta) - argus_G(c, tb));
     }
     case Kind::Chebychev: {  // full range: (hi-lo)/2 (2 + sum_{k even} a_k 2/(1-k^2))

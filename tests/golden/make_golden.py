@@ -19,6 +19,8 @@ Fixtures (all float64, bit-exact from the reference build):
                      proj/src/eval.cpp:40-86) -- cross-check, not bitwise
   argus_mp.json      ArgusBG (p = 1/2) normalisation integrals by mpmath quadrature
                      at 50 digits (closed-form pin)
+  ref_fits.json      reference Nelder-Mead fits (proj/src/fit.cpp:86-251, tolerance
+                     1e-10) on seeded data: fitted values, uncertainties, NLL minimum
 """
 from __future__ import annotations
 
@@ -32,7 +34,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 
 from oracle.oracle import RefDataset, RefModel, build, ref_rng_gauss, ref_rng_uniform  # noqa: E402
-from tests.models import EXPR_MODELS, REF_MODELS  # noqa: E402
+from tests.models import EXPR_MODELS, FIT_CASES, REF_MODELS  # noqa: E402
 
 N_EVENTS = 4096
 
@@ -88,6 +90,29 @@ def main():
         cases.append(dict(m0=m0, c=c, lo=lo, hi=hi, integral=float(val)))
     with open(os.path.join(HERE, "argus_mp.json"), "w") as fh:
         json.dump(cases, fh, indent=1)
+    fits = {}
+    for name, case in FIT_CASES.items():
+        gen = RefModel(case["ref_text"])
+        for k, v in case.get("truth", {}).items():
+            gen.set(k, v)
+        if case.get("data_from") == "oracle":
+            from oracle.oracle import OracleModel
+            o = OracleModel(case["ours_text"])
+            for k, v in case.get("truth", {}).items():
+                o.set(k, v)
+            (xs,), _ = o.sample(case["n"], case["seed"])
+        else:
+            xs, _ = gen.sample(case["n"], case["seed"])
+        ds = RefDataset(case["column"], xs)
+        fit = RefModel(case["ref_text"])
+        for k, v in case.get("start", {}).items():
+            fit.set(k, v)
+        r = fit.fit(ds, RefModel.PRECISE, tol=case["tol"])
+        r["params"] = {k: list(fit.get(k)) for k in case["free"]}
+        fits[name] = r
+        print("fit", name, r)
+    with open(os.path.join(HERE, "ref_fits.json"), "w") as fh:
+        json.dump(fits, fh, indent=1)
     print("golden fixtures written to", HERE)
 
 

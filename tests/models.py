@@ -157,3 +157,25 @@ parameter a2 0.1 -1 1
 pdf po Polynomial(x, a1, a2)
 """, 13, "x"),
 }
+
+GAUSS_CLOSURE = """
+observable x -6 6
+parameter mu 0 -3 3
+parameter sigma 1.2 0.1 4
+pdf g Gaussian(x, mu, sigma)
+"""
+
+# Reference Nelder-Mead fits pinned as golden values (tests/golden/ref_fits.json).
+# mix_acceptance: proj/tests/acceptance.cpp:122-135 (criterion 3 data);
+# gauss_closure: proj/tests/acceptance.cpp:226-250 (criterion 8);
+# argus_mix: the config-2 model (ArgusBG as the reference's Expression).
+FIT_CASES = {
+    "mix_acceptance": dict(ref_text=MIX, ours_text=MIX, n=20000, seed=314159, column="x", tol=1e-10,
+                           free=["mu", "sigma", "c", "f"]),
+    "gauss_closure": dict(ref_text=GAUSS_CLOSURE, ours_text=GAUSS_CLOSURE, n=50000, seed=424242, column="x",
+                          tol=1e-10, truth={"mu": 0.5, "sigma": 1.0}, start={"mu": 0.0, "sigma": 1.2},
+                          free=["mu", "sigma"]),
+    "argus_mix": dict(ref_text=ARGUS_REF, ours_text=ARGUS_OURS, n=20000, seed=99, column="x", tol=1e-10,
+                      data_from="oracle", start={"m": 5.2785, "s": 0.0032, "c": -18.0, "f": 0.12},
+                      free=["m", "s", "c", "f"]),
+}

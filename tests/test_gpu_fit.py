@@ -1,0 +1,87 @@
+"""Fit drivers on the GPU likelihood against the reference's own fits (golden values
+from tests/golden/ref_fits.json, produced by the unmodified reference Nelder-Mead,
+proj/src/fit.cpp:86-251).  Target (BASELINE north_star): fitted parameters within 1e-6.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_2003_12875_b200 as fb
+from oracle.oracle import OracleModel
+from tests.models import FIT_CASES
+
+pytestmark = pytest.mark.gpu
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "ref_fits.json")))
+
+
+def data_for(case):
+    gen = fb.Model.from_string(case["ours_text"])
+    for k, v in case.get("truth", {}).items():
+        gen.set(k, v)
+    cols, _ = fb.sample_host(gen, case["n"], case["seed"])
+    return fb.DataSet.from_columns(cols), cols
+
+
+def start_model(case):
+    m = fb.Model.from_string(case["ours_text"])
+    for k, v in case.get("start", {}).items():
+        m.set(k, v)
+    return m
+
+
+@pytest.mark.parametrize("name", list(FIT_CASES))
+def test_nelder_mead_matches_reference_fit(name):
+    case, gold = FIT_CASES[name], GOLD[name]
+    ds, _ = data_for(case)
+    m = start_model(case)
+    r = fb.fit_to(m, ds, tolerance=case["tol"])
+    assert r.converged and gold["converged"]
+    assert r.uncertainties_valid
+    for p in r.parameters:
+        want, unc = gold["params"][p.name]
+        assert abs(p.value - want) <= 1e-6, (p.name, p.value, want)
+        assert p.uncertainty == pytest.approx(unc, rel=1e-3)
+        assert m.get(p.name)[0] == p.value  # written back (proj/src/fit.cpp:228-246)
+    assert abs(r.nll_min - gold["nll"]) <= 1e-12 * abs(gold["nll"]) + 1e-9
+    assert r.n_launches < r.n_nll_calls  # independent points were batched
+
+
+@pytest.mark.parametrize("name", list(FIT_CASES))
+def test_gradient_fit_reaches_reference_minimum(name):
+    case, gold = FIT_CASES[name], GOLD[name]
+    ds, _ = data_for(case)
+    m = start_model(case)
+    r = fb.fit_gradient(m, ds, tolerance=1e-12, max_iterations=200)
+    assert r.converged
+    for p in r.parameters:
+        want, unc = gold["params"][p.name]
+        assert abs(p.value - want) <= max(1e-6, 2e-3 * unc), (p.name, p.value, want)
+    assert r.nll_min <= gold["nll"] + 1e-7
+    d = len(r.parameters)
+    # every iteration is one launch of 2d+1 points (plus the one Hessian launch)
+    assert r.n_nll_calls == (r.n_launches - 1) * (2 * d + 1) + (1 + 2 * d + 2 * d * (d - 1))
+
+
+def test_fit_nll_matches_oracle_at_minimum():
+    case = FIT_CASES["argus_mix"]
+    ds, cols = data_for(case)
+    m = start_model(case)
+    r = fb.fit_to(m, ds, tolerance=case["tol"])
+    o = OracleModel(case["ours_text"])
+    th = m.theta()
+    _, comp, _ = o.nll([cols["x"]], th)
+    assert abs(r.nll_min - comp) <= 1e-12 * abs(comp)
+
+
+def test_hessian_points_batched_into_one_launch():
+    case = FIT_CASES["gauss_closure"]
+    ds, _ = data_for(case)
+    m = start_model(case)
+    r = fb.fit_to(m, ds, tolerance=1e-8)
+    gold = GOLD["gauss_closure"]
+    for p in r.parameters:
+        assert abs(p.value - gold["params"][p.name][0]) <= 5 * p.uncertainty * 1e-3 + 1e-6
+    assert np.isfinite(r.nll_min)

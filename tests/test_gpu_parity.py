@@ -1,0 +1,353 @@
+"""GPU parity of the fused sm_100a path, through the C ABI, against the oracle and the
+reference's own golden vectors.
+
+Tolerances (BASELINE.json north_star): per-event PDF values within 1e-13 relative;
+|dNLL|/|NLL| <= 1e-12 against the compensated (Neumaier) oracle sum.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import paper_2003_12875_b200 as fb
+from paper_2003_12875_b200 import configs
+from paper_2003_12875_b200 import distributed as D
+from oracle.oracle import OracleModel
+from tests.models import ARGUS_OURS, EXPR_MODELS, MIX, REF_MODELS
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+PER_EVENT = 1e-13
+NLL_TOL = 1e-12
+
+
+def rel(a, b):
+    return np.max(np.abs(np.asarray(a) - np.asarray(b)) / np.abs(np.asarray(b)))
+
+
+def setup(text, n, seed):
+    m = fb.Model.from_string(text)
+    cols, _ = fb.sample_host(m, n, seed)
+    ds = fb.DataSet.from_columns(cols)
+    return m, ds, [cols[k] for k in m.observables], OracleModel(text)
+
+
+# ------------------------------------------------------------------ golden vectors
+
+@pytest.mark.parametrize("name", list(REF_MODELS))
+def test_golden_reference_models(name):
+    """GPU vs the REFERENCE's own per-event values and compensated NLL (golden)."""
+    text, _ = REF_MODELS[name]
+    g = np.load(os.path.join(GOLD, "ref_models.npz"))
+    x, p, sc = g[f"{name}/x"], g[f"{name}/p"], g[f"{name}/scalars"]
+    m = fb.Model.from_string(text)
+    ds = fb.DataSet.from_columns({"x": x})
+    assert rel(fb.probabilities(m, ds), p) <= PER_EVENT
+    v = fb.nll(m, ds)
+    assert abs(v.value - sc[1]) <= NLL_TOL * abs(sc[1])
+    assert abs(v.value - sc[0]) <= NLL_TOL * abs(sc[0])  # the reference's naive nll() too
+    assert v.first_invalid == -1
+
+
+@pytest.mark.parametrize("name", list(EXPR_MODELS))
+def test_golden_expression_route(name):
+    """Restated kinds vs the reference's Expression + Simpson route (golden)."""
+    _, ours, _, col = EXPR_MODELS[name]
+    g = np.load(os.path.join(GOLD, "expr_models.npz"))
+    x, p, sc = g[f"{name}/x"], g[f"{name}/p"], g[f"{name}/scalars"]
+    m = fb.Model.from_string(ours)
+    ds = fb.DataSet.from_columns({col: x})
+    assert rel(fb.probabilities(m, ds), p) <= PER_EVENT
+    assert abs(fb.nll(m, ds).value - sc[0]) <= NLL_TOL * abs(sc[0])
+
+
+# ------------------------------------------------------------------ oracle parity
+
+ALL = {**{k: v[0] for k, v in REF_MODELS.items()}, **{k: v[1] for k, v in EXPR_MODELS.items()},
+       **{w.name: w.text for w in configs.BY_INDEX[:4]}}
+
+
+@pytest.mark.parametrize("name", list(ALL))
+def test_oracle_parity_per_event_and_nll(name):
+    m, ds, cols, o = setup(ALL[name], 100_003, 12345)
+    assert rel(fb.probabilities(m, ds), o.probabilities(cols)) <= PER_EVENT
+    v = fb.nll(m, ds)
+    _, comp, bad = o.nll(cols)
+    assert v.first_invalid == bad == -1
+    assert abs(v.value - comp) <= NLL_TOL * abs(comp)
+
+
+@pytest.mark.parametrize("w", configs.BY_INDEX[:4], ids=lambda w: w.name)
+def test_multi_point_launch_parity(w):
+    m, ds, cols, o = setup(w.text, 200_000, w.data_seed)
+    pts = w.points(m, n_points=min(w.n_points, 24))
+    vals, bad, launches = fb.nll_points(m, ds, pts)
+    assert launches == 2  # one fused kernel + one fixed-order fold, independent of N and P
+    for p in range(len(pts)):
+        _, comp, ob = o.nll(cols, pts[p])
+        assert bad[p] == ob == -1
+        assert abs(vals[p] - comp) <= NLL_TOL * abs(comp), p
+
+
+def test_points_are_independent_of_batching():
+    """A point's value does not depend on the other points of the launch (bitwise)."""
+    w = configs.C2
+    m, ds, _, _ = setup(w.text, 300_001, 7)
+    pts = w.points(m, n_points=40)
+    full, _, _ = fb.nll_points(m, ds, pts)
+    for p in (0, 13, 39):
+        one, _, _ = fb.nll_points(m, ds, pts[p:p + 1])
+        assert one[0] == full[p]
+    again, _, _ = fb.nll_points(m, ds, pts)
+    assert np.array_equal(again, full)  # deterministic run to run
+
+
+def test_more_than_512_points_split_launches():
+    w = configs.C1
+    m, ds, cols, o = setup(w.text, 20_000, 3)
+    pts = w.points(m, n_points=1100)
+    vals, bad, launches = fb.nll_points(m, ds, pts)
+    assert launches == 6
+    for p in (0, 511, 512, 1099):
+        assert abs(vals[p] - o.nll(cols, pts[p])[1]) <= NLL_TOL * abs(vals[p])
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 255, 2047, 2048, 2049, 4095, 4097, 10007])
+def test_tile_boundaries_and_ragged_tails(n):
+    m, ds, cols, o = setup(ARGUS_OURS, n, 11)
+    assert rel(fb.probabilities(m, ds), o.probabilities(cols)) <= PER_EVENT
+    v = fb.nll(m, ds)
+    assert abs(v.value - o.nll(cols)[1]) <= NLL_TOL * abs(o.nll(cols)[1])
+
+
+def test_misaligned_device_view_uses_cooperative_staging():
+    """A slice starting at an odd index is 8- but not 16-byte aligned: no bulk copy."""
+    m, ds, cols, o = setup(MIX, 50_001, 5)
+    for b, e in ((1, 50_001), (3, 40_000), (2048 + 1, 2048 * 5 + 3)):
+        sub = ds.slice(b, e)
+        v = fb.nll(m, sub)
+        _, comp, _ = o.nll([cols[0][b:e]])
+        assert abs(v.value - comp) <= NLL_TOL * abs(comp)
+
+
+def test_empty_dataset():
+    m = fb.Model.from_string(MIX)
+    ds = fb.DataSet.from_columns({"x": np.zeros(0)})
+    v = fb.nll(m, ds)
+    assert v.value == 0.0 and v.n_entries == 0  # proj/tests/test_eval.cpp:92-100
+    ext = fb.Model.from_string(configs.C4.text)
+    th = ext.theta()
+    nu = sum(th[ext.param_names.index(k)] for k in ("n1", "n2", "n3", "n4", "n5", "nb"))
+    assert fb.nll(ext, ds).value == pytest.approx(nu, rel=1e-15)
+
+
+def test_invalid_events_report_first_index():
+    # ArgusBG is zero for x >= m0: events at the top of the range are invalid
+    text = EXPR_MODELS["argus_only"][1].replace("parameter m0 5.291 5.0 5.4 const",
+                                                 "parameter m0 5.285 5.0 5.4 const")
+    m = fb.Model.from_string(text)
+    o = OracleModel(text)
+    rng = np.random.default_rng(1)
+    x = rng.uniform(5.20, 5.284, 30000)
+    x[17011] = 5.2875  # beyond m0
+    x[23000] = 5.289
+    ds = fb.DataSet.from_columns({"x": x})
+    v = fb.nll(m, ds)
+    _, comp, bad = o.nll([x])
+    assert math.isinf(v.value) and v.first_invalid == bad
+    # NaN data are invalid too (proj/src/eval.cpp:138-145)
+    x2 = rng.uniform(5.20, 5.28, 5000)
+    x2[4321] = np.nan
+    v = fb.nll(m, fb.DataSet.from_columns({"x": x2}))
+    assert math.isinf(v.value) and v.first_invalid == 4321
+
+
+def test_zero_density_chisquare_first_invalid():  # proj/tests/test_eval.cpp:205-217
+    m = fb.Model.from_string("observable x 0 20\nparameter k 4 0.5 20\npdf c ChiSquare(x, k)\n")
+    v = fb.nll(m, fb.DataSet.from_columns({"x": np.array([1.0, 0.0, 2.0])}))
+    assert math.isinf(v.value) and v.first_invalid == 1
+
+
+def test_single_entry_closed_form():  # proj/tests/test_eval.cpp:80-90
+    m = fb.Model.from_string("observable x -10 10\nparameter mu 0 -5 5\nparameter sigma 1 0.1 5\n"
+                             "pdf g Gaussian(x, mu, sigma)\n")
+    v = fb.nll(m, fb.DataSet.from_columns({"x": np.array([0.0])}))
+    assert v.value == pytest.approx(-math.log(1.0 / math.sqrt(2.0 * math.pi)), rel=1e-12)
+
+
+def test_eval_batch_per_pdf():
+    """PdfSpec::eval_batch of sub-pdfs (unnormalised; mixture components normalised)."""
+    text = REF_MODELS["mix3_nested"][0]
+    m, ds, cols, o = setup(text, 30_000, 4)
+    names = m.pdf_names
+    for node, name in enumerate(names):
+        got = fb.eval_batch(m, name, ds)
+        want = o.eval_batch(node, cols)
+        assert rel(got, want) <= PER_EVENT, name
+
+
+def test_sum_of_products_and_nested_sums():
+    text = """
+observable x -5 5
+observable y 0 10
+parameter m 0.2 -1 1
+parameter s 1.1 0.1 3
+parameter c -0.5 -2 0
+parameter c2 -0.1 -2 0
+parameter a1 0.1 -1 1
+parameter f 0.3 0 1
+parameter g 0.6 0 1
+pdf gx Gaussian(x, m, s)
+pdf ey Exponential(y, c)
+pdf ex Exponential(x, c2)
+pdf py Polynomial(y, a1)
+pdf ey2 Exponential(y, c2)
+pdf ymix AddPdf(py, g, ey2)
+pdf sig ProdPdf(gx, ey)
+pdf bkg ProdPdf(ex, ymix)
+pdf model AddPdf(sig, f, bkg)
+"""
+    m = fb.Model.from_string(text)
+    o = OracleModel(text)
+    rng = np.random.default_rng(2)
+    cols = [rng.uniform(-5, 5, 40_000), rng.uniform(0, 10, 40_000)]
+    ds = fb.DataSet.from_columns({"x": cols[0], "y": cols[1]})
+    assert rel(fb.probabilities(m, ds), o.probabilities(cols)) <= PER_EVENT
+    assert abs(fb.nll(m, ds).value - o.nll(cols)[1]) <= NLL_TOL * abs(o.nll(cols)[1])
+
+
+def test_extended_model_parity():
+    w = configs.C4
+    m, ds, cols, o = setup(w.text, 150_000, 77)
+    pts = w.points(m, n_points=6)
+    vals, _, _ = fb.nll_points(m, ds, pts)
+    for p in range(6):
+        _, comp, _ = o.nll(cols, pts[p])
+        assert abs(vals[p] - comp) <= NLL_TOL * abs(comp)
+
+
+def test_launch_count_independent_of_n():  # proj/tests/test_eval.cpp:191-203
+    m = fb.Model.from_string(MIX)
+    small = fb.nll(m, fb.DataSet.from_columns({"x": np.full(100, 0.5)}))
+    large = fb.nll(m, fb.DataSet.from_columns({"x": np.full(100000, 0.5)}))
+    assert small.n_evaluations == large.n_evaluations == 2
+    before = fb.kernel_launches()
+    fb.nll(m, fb.DataSet.from_columns({"x": np.full(10, 0.5)}))
+    assert fb.kernel_launches() - before == 2
+
+
+def test_device_view_over_torch_tensors():
+    import torch
+    w = configs.C3
+    m = fb.Model.from_string(w.text)
+    cols, _ = fb.sample_host(m, 70_001, 5)
+    tens = {k: torch.from_numpy(cols[k]).cuda() for k in m.observables}
+    ds = fb.DataSet.from_device(tens, device=0)
+    o = OracleModel(w.text)
+    _, comp, _ = o.nll([cols[k] for k in m.observables])
+    assert abs(fb.nll(m, ds).value - comp) <= NLL_TOL * abs(comp)
+
+
+def test_c_abi_entry_points():
+    m = fb.Model.from_string(MIX)
+    ds, eff = fb.DataSet.sample(m, 20000, 314159)
+    assert eff == -1.0 and ds.n_rows == 20000
+    value, nev = fb.nll_c(m, ds, fb.EvalMode.Gpu)
+    assert nev == 2
+    v2, _ = fb.nll_c(m, ds, fb.EvalMode.BatchPrecise)
+    assert v2 == value
+    with pytest.raises(fb.FfitError) as e:
+        fb.nll_c(m, ds, fb.EvalMode.Scalar)
+    assert e.value.code == 1
+    o = OracleModel(MIX)
+    x = ds.column("x")
+    assert abs(value - o.nll([x])[1]) <= NLL_TOL * abs(value)
+    m.set("sigma", 1.5)
+    assert fb.nll_c(m, ds)[0] != value
+
+
+def test_csv_round_trip(tmp_path):
+    m = fb.Model.from_string(MIX)
+    ds, _ = fb.DataSet.sample(m, 3000, 1)
+    p = str(tmp_path / "d.csv")
+    ds.write_csv(p)
+    with open(p, "a") as fh:
+        fh.write("7.5\n")  # outside [-5, 5]: dropped (proj/src/dataset.cpp:104-112)
+    back, dropped = fb.DataSet.read_csv(m, p)
+    assert dropped == 1 and np.array_equal(back.column("x"), ds.column("x"))
+
+
+def test_combine_kernel_matches_host_combine():
+    import torch
+    rng = np.random.default_rng(3)
+    pairs = np.zeros((3, 17, 2))
+    pairs[..., 0] = rng.normal(-2e7, 1e4, (3, 17))
+    pairs[..., 1] = rng.normal(0, 1e-8, (3, 17))
+    d_in = torch.from_numpy(pairs).cuda()
+    d_out = torch.zeros((17, 2), dtype=torch.float64, device="cuda")
+    fb.ffit.combine_pairs_device(d_in.data_ptr(), 3, 17, d_out.data_ptr())
+    torch.cuda.synchronize()
+    assert np.array_equal(d_out.cpu().numpy(), D.combine_pairs(pairs))
+
+
+def test_sharded_single_rank_equals_direct():
+    import torch.distributed as dist
+    w = configs.C2
+    m, ds, _, _ = setup(w.text, 100_000, 5)
+    pts = w.points(m, n_points=5)
+    sh = D.ShardedNll(m, ds, ds.n_rows, 0, dist, 0)
+    vals = sh.nll_points(pts)
+    direct, _, _ = fb.nll_points(m, ds, pts)
+    assert np.array_equal(vals, direct)
+
+
+def test_shard_sum_equals_whole():
+    """Additivity over event shards (the multi-GPU decomposition), exact to 1e-12."""
+    w = configs.C2
+    m, ds, _, _ = setup(w.text, 1_000_003, 21)
+    pts = w.points(m, n_points=3)
+    whole, _, _ = fb.nll_points(m, ds, pts)
+    parts = []
+    for r in range(4):
+        b, e = D.shard_bounds(ds.n_rows, 4, r)
+        parts.append(fb.nll_points_partial(m, ds.slice(b, e), pts)[0])
+    comb = D.combine_pairs(np.stack(parts))
+    assert np.all(np.abs(comb.sum(axis=1) - whole) <= NLL_TOL * np.abs(whole))
+
+
+# ------------------------------------------------------------------ full BASELINE sizes
+
+@pytest.mark.slow
+def test_c2_full_size_parity_and_properties():
+    """configs[1] at 1e7 events: oracle parity at two points, shard additivity and
+    permutation invariance at all sizes the oracle cannot afford."""
+    w = configs.C2
+    m, ds, cols, o = setup(w.text, w.n_events, w.data_seed)
+    pts = w.points(m)
+    vals, bad, _ = fb.nll_points(m, ds, pts)
+    assert np.all(bad == -1) and np.all(np.isfinite(vals))
+    for p in (0, 199):
+        _, comp, _ = o.nll(cols, pts[p])
+        assert abs(vals[p] - comp) <= NLL_TOL * abs(comp)
+    perm = np.random.default_rng(0).permutation(w.n_events)
+    shuffled = fb.DataSet.from_columns({"x": cols[0][perm]})
+    sv, _, _ = fb.nll_points(m, shuffled, pts[:8])
+    assert np.all(np.abs(sv - vals[:8]) <= NLL_TOL * np.abs(vals[:8]))
+
+
+@pytest.mark.slow
+def test_c3_full_size_three_columns():
+    w = configs.C3
+    m, ds, cols, o = setup(w.text, w.n_events, w.data_seed)
+    pts = w.points(m, n_points=4)
+    vals, bad, _ = fb.nll_points(m, ds, pts)
+    assert np.all(bad == -1)
+    half = w.n_events // 2
+    a = fb.nll_points_partial(m, ds.slice(0, half), pts)[0]
+    b = fb.nll_points_partial(m, ds.slice(half, w.n_events), pts)[0]
+    comb = D.combine_pairs(np.stack([a, b])).sum(axis=1)
+    assert np.all(np.abs(comb - vals) <= NLL_TOL * np.abs(vals))
+    _, comp, _ = o.nll(cols, pts[0])
+    assert abs(vals[0] - comp) <= NLL_TOL * abs(comp)
