@@ -175,7 +175,7 @@ FIT_CASES = {
     "gauss_closure": dict(ref_text=GAUSS_CLOSURE, ours_text=GAUSS_CLOSURE, n=50000, seed=424242, column="x",
                           tol=1e-10, truth={"mu": 0.5, "sigma": 1.0}, start={"mu": 0.0, "sigma": 1.2},
                           free=["mu", "sigma"]),
-    "argus_mix": dict(ref_text=ARGUS_REF, ours_text=ARGUS_OURS, n=20000, seed=99, column="x", tol=1e-10,
+    "argus_mix": dict(ref_text=ARGUS_REF, ours_text=ARGUS_OURS, n=20000, seed=99, column="x", tol=1e-12,
                       data_from="oracle", start={"m": 5.2785, "s": 0.0032, "c": -18.0, "f": 0.12},
                       free=["m", "s", "c", "f"]),
 }
