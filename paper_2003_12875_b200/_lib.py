@@ -88,6 +88,7 @@ SIGNATURES = {
     "ffcu_kernel_timer": (I, [I]),
     "ffcu_kernel_timer_read": (I, [DP, ULLP]),
     "ffcu_fp64_peak": (I, [DP, ctypes.POINTER(ctypes.c_float)]),
+    "ffcu_math_probe": (I, [I, DP, DP, LL]),
     "ffcu_sample_host": (I, [VP, LL, ULL, ctypes.POINTER(DP), DP]),
 }
 

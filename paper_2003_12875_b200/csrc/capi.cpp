@@ -701,6 +701,25 @@ FFB_API int ffcu_kernel_timer_read(double* total_ms, unsigned long long* count) 
   });
 }
 
+FFB_API int ffcu_math_probe(int which, const double* in, double* out, long long n) {
+  return guarded([&] {
+    require(in, "in");
+    require(out, "out");
+    if (which < 0 || which > 1) ffb::usage_error("which must be 0 (exp) or 1 (log)");
+    if (n <= 0) return;
+    double *d_in = nullptr, *d_out = nullptr;
+    const std::size_t bytes = static_cast<std::size_t>(n) * sizeof(double);
+    ffb::cuda_check(cudaMalloc(&d_in, bytes), "cudaMalloc");
+    ffb::cuda_check(cudaMalloc(&d_out, bytes), "cudaMalloc");
+    cudaMemcpy(d_in, in, bytes, cudaMemcpyHostToDevice);
+    ffb::count_launches(ffb::launch_math_probe(which, d_in, d_out, n, nullptr));
+    const cudaError_t e = cudaMemcpy(out, d_out, bytes, cudaMemcpyDeviceToHost);
+    cudaFree(d_in);
+    cudaFree(d_out);
+    ffb::cuda_check(e, "math_probe");
+  });
+}
+
 FFB_API int ffcu_fp64_peak(double* fma_per_s, float* ms) {
   return guarded([&] {
     require(fma_per_s, "fma_per_s");

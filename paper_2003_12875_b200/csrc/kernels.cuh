@@ -41,11 +41,17 @@ std::size_t nll_scratch_bytes(long long n, int P, int ncols);
 //   partials, then a deterministic fixed-order pass over the partials.
 // out[p] = (s, c) with NLL_events(p) = s + c; bad[p] = smallest event index with
 // p <= 0 or non-finite (kNoInvalid if none).  `scratch` holds nll_scratch_bytes.
-// ev_start / ev_stop (may be null) are recorded around the fused kernel alone.
+// `full` selects the kernel build with every leaf kind and the general ArgusBG
+// path (plan_needs_full); ev_start / ev_stop (may be null) are recorded around
+// the fused kernel alone.
 NllLaunchInfo launch_nll(const DevPlan& plan, const ColPtrs& cols, long long n,
                          const double* d_consts, int P, void* scratch, SumPair* d_out,
-                         unsigned long long* d_bad, cudaStream_t stream,
+                         unsigned long long* d_bad, cudaStream_t stream, bool full,
                          cudaEvent_t ev_start = nullptr, cudaEvent_t ev_stop = nullptr);
+
+// True when the plan uses ChiSquare / JohnsonSU, or an ArgusBG point has p != 1/2
+// or |c| > 700 (host_consts: the P constant rows about to be launched).
+bool plan_needs_full(const DevPlan& plan, const double* host_consts, int P);
 
 // Per-event values of the plan for one point (probabilities() when the plan is
 // normalised, PdfSpec::eval_batch when not).
@@ -55,6 +61,9 @@ int launch_eval(const DevPlan& plan, const ColPtrs& cols, long long n, const dou
 // Combine R per-rank Neumaier pairs per point in fixed rank order (multi-GPU
 // exchange step after an all-gather): in = R x P pairs, out = P pairs.
 int launch_combine_ranks(const SumPair* d_in, int R, int P, SumPair* d_out, cudaStream_t stream);
+
+// Test hook: which = 0 -> the kernel's exp, 1 -> its log, over n device doubles.
+int launch_math_probe(int which, const double* d_in, double* d_out, long long n, cudaStream_t stream);
 
 // DFMA-chain microbenchmark: returns FP64 FMA instructions per second measured
 // with CUDA events on `stream` (the FP64 roofline denominator).

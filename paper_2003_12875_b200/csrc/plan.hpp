@@ -26,7 +26,7 @@ enum LeafKind : int {
   LK_EXPO = 1,     // c: [coef, c]
   LK_CHISQ = 2,    // c: [coef, k/2 - 1, at_zero]
   LK_JOHNSON = 3,  // c: [coef, mu, 1/lambda, gamma, delta, delta/(lambda sqrt(2 pi))]
-  LK_ARGUS = 4,    // c: [coef, m0, c, p]
+  LK_ARGUS = 4,    // c: [coef, m0, c, p, 1/m0]
   LK_CHEB = 5,     // c: [coef, lo+hi, 1/(hi-lo), a1..an]
   LK_POLY = 6,     // c: [coef, a1..an]
 };

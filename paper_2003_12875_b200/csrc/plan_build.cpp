@@ -73,6 +73,7 @@ struct Emitter {
         consts.push_back(par(p, 0));
         consts.push_back(par(p, 1));
         consts.push_back(par(p, 2));
+        consts.push_back(theta ? 1.0 / par(p, 0) : 0.0);  // hoisted reciprocal of m0
         break;
       case Kind::Chebychev: {
         t.kind = LK_CHEB;
@@ -190,6 +191,13 @@ HostPlan compile_plan(const Model& m, int pdf, bool normalized) {
 }
 
 void build_constants(const HostPlan& plan, const Model& m, const double* theta, double* row) {
+  for (std::size_t i = 0; i < m.params.size(); ++i) {
+    // the device exp assumes finite arguments (fastmath.cuh); the reference's
+    // set_value range check excludes NaN / inf the same way (proj/src/graph.cpp:121)
+    if (!std::isfinite(theta[i])) {
+      numeric_error("non-finite value for parameter '" + m.params[i].name + "'");
+    }
+  }
   m.check_params(plan.pdf, theta);
   const double scale = plan.normalized ? 1.0 / m.normalization(plan.pdf, theta) : 1.0;
   Emitter e{m, theta, {}, {}, {}};

@@ -407,6 +407,14 @@ def fp64_peak():
     return v.value, ms.value
 
 
+def math_probe(which: str, x) -> np.ndarray:
+    """The fused kernel's device exp ("exp") or log ("log") over an array (test hook)."""
+    x = _f64(x)
+    out = np.empty_like(x)
+    _check(lib().ffcu_math_probe({"exp": 0, "log": 1}[which], _dp(x), _dp(out), len(x)))
+    return out
+
+
 def sample_host(model: Model, n: int, seed: int):
     """Seeded generator into host arrays, one per observable (name -> array)."""
     names = model.observables

@@ -164,6 +164,47 @@ def test_invalid_events_report_first_index():
     assert math.isinf(v.value) and v.first_invalid == 4321
 
 
+@pytest.mark.parametrize("p,c", [(0.7, -20.0), (0.5, -800.0), (0.5, 3.0), (1.3, 750.0)])
+def test_argus_general_path(p, c):
+    """ArgusBG off the fast domain (p != 1/2 or |c| > 700) runs the full kernel build
+    (pow, range-checked exp) and Simpson normalisation on the host."""
+    text = f"""
+observable x 5.2 5.29
+parameter m0 5.291 5.0 5.4 const
+parameter c {c} -1000 1000
+parameter p {p} 0 3
+pdf bkg ArgusBG(x, m0, c, p)
+"""
+    m = fb.Model.from_string(text)
+    o = OracleModel(text)
+    x = np.random.default_rng(4).uniform(5.2, 5.2905, 20000)
+    ds = fb.DataSet.from_columns({"x": x})
+    assert rel(fb.probabilities(m, ds), o.probabilities([x])) <= PER_EVENT
+    assert abs(fb.nll(m, ds).value - o.nll([x])[1]) <= NLL_TOL * abs(o.nll([x])[1])
+
+
+def test_non_finite_data_and_parameters():
+    """Non-finite data make the event invalid (as the reference's arithmetic does);
+    non-finite parameter values are rejected before any launch."""
+    m = fb.Model.from_string(MIX)
+    o = OracleModel(MIX)
+    x = np.random.default_rng(9).uniform(-5, 5, 10000)
+    for bad_value in (np.inf, -np.inf, np.nan):
+        y = x.copy()
+        y[777] = bad_value
+        y[9000] = bad_value
+        v = fb.nll(m, fb.DataSet.from_columns({"x": y}))
+        _, comp, ob = o.nll([y])
+        assert math.isinf(v.value) and v.first_invalid == ob == 777
+        p = fb.probabilities(m, fb.DataSet.from_columns({"x": y}))
+        assert math.isnan(p[777]) and np.all(np.isfinite(np.delete(p, [777, 9000])))
+    pts = m.theta()[None, :].copy()
+    pts[0, m.param_names.index("mu")] = np.nan
+    with pytest.raises(fb.FfitError) as e:
+        fb.nll_points(m, fb.DataSet.from_columns({"x": x}), pts)
+    assert e.value.code == 3
+
+
 def test_zero_density_chisquare_first_invalid():  # proj/tests/test_eval.cpp:205-217
     m = fb.Model.from_string("observable x 0 20\nparameter k 4 0.5 20\npdf c ChiSquare(x, k)\n")
     v = fb.nll(m, fb.DataSet.from_columns({"x": np.array([1.0, 0.0, 2.0])}))

@@ -139,11 +139,11 @@ def test_point_constants_fold_normalisations():
     n_sig = o.normalization(node=0)
     n_bkg = o.normalization(node=1)
     n_mod = o.normalization()
-    # [coef_g, mu, -1/(2s^2), coef_a, m0, c, p]
+    # [coef_g, mu, -1/(2s^2), coef_a, m0, c, p, 1/m0]
     assert row[1] == v["m"] and row[2] == -1.0 / (2.0 * v["s"] * v["s"])
     assert row[0] == pytest.approx((v["f"] / n_sig) / n_mod, rel=2e-16)
     assert row[3] == pytest.approx(((1 - v["f"]) / n_bkg) / n_mod, rel=2e-16)
-    assert list(row[4:]) == [v["m0"], v["c"], v["p"]]
+    assert list(row[4:]) == [v["m0"], v["c"], v["p"], 1.0 / v["m0"]]
 
 
 @pytest.mark.parametrize("name", list(REF_MODELS) + list(EXPR_MODELS))
