@@ -185,7 +185,7 @@ int ffcu_kernel_timer(int enable);
 int ffcu_kernel_timer_read(double* total_ms, unsigned long long* count);
 /* Kernels this library has launched in this process. */
 unsigned long long ffcu_kernel_launches(void);
-/* Test hook: the fused kernel's device exp (which = 0) or log (1) over n host doubles. */
+/* Test hook: the fused kernel's device exp (0), log (1), sqrt (2) or rsqrt seed (3) over n host doubles. */
 int ffcu_math_probe(int which, const double* in, double* out, long long n);
 /* Measured FP64 FMA instructions per second on the current device. */
 int ffcu_fp64_peak(double* fma_per_s, float* ms);

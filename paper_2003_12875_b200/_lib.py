@@ -10,7 +10,11 @@ import os
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libffit_b200.so")
+# FFB_LIB_VARIANT=<tag> loads lib/ab/libffit_b200_<tag>.so instead (A/B builds of the
+# same sources with different -D switches, csrc/Makefile `ab` target)
+_variant = os.environ.get("FFB_LIB_VARIANT")
+LIB_PATH = (os.path.join(HERE, "lib", "ab", f"libffit_b200_{_variant}.so") if _variant
+            else os.path.join(HERE, "lib", "libffit_b200.so"))
 CSRC = os.path.join(HERE, "csrc")
 
 D = ctypes.c_double

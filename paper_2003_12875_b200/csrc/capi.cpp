@@ -705,7 +705,7 @@ FFB_API int ffcu_math_probe(int which, const double* in, double* out, long long 
   return guarded([&] {
     require(in, "in");
     require(out, "out");
-    if (which < 0 || which > 1) ffb::usage_error("which must be 0 (exp) or 1 (log)");
+    if (which < 0 || which > 3) ffb::usage_error("which must be 0 (exp), 1 (log), 2 (sqrt), 3 (rsqrt seed)");
     if (n <= 0) return;
     double *d_in = nullptr, *d_out = nullptr;
     const std::size_t bytes = static_cast<std::size_t>(n) * sizeof(double);

@@ -280,8 +280,8 @@ int Engine::nll_points_device(const DeviceDataset& ds, const double* thetas, int
         g_timer_events.emplace_back(ea, eb);
       }
     }
-    const bool full = plan_needs_full(plan_.dev, h_consts_[slot_], P);
-    last_ = launch_nll(plan_.dev, cols, ds.n, d_consts, P, d_scratch_, d_pairs, d_bad, s, full, ea, eb);
+    const int ks = plan_kind_set(plan_.dev, h_consts_[slot_], P);
+    last_ = launch_nll(plan_.dev, cols, ds.n, d_consts, P, d_scratch_, d_pairs, d_bad, s, ks, ea, eb);
     launches = last_.launches;
     cuda_check(cudaGetLastError(), "launch_nll");
   }

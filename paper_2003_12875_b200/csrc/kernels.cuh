@@ -41,17 +41,17 @@ std::size_t nll_scratch_bytes(long long n, int P, int ncols);
 //   partials, then a deterministic fixed-order pass over the partials.
 // out[p] = (s, c) with NLL_events(p) = s + c; bad[p] = smallest event index with
 // p <= 0 or non-finite (kNoInvalid if none).  `scratch` holds nll_scratch_bytes.
-// `full` selects the kernel build with every leaf kind and the general ArgusBG
-// path (plan_needs_full); ev_start / ev_stop (may be null) are recorded around
-// the fused kernel alone.
+// `ks` selects the kernel build by the leaf kinds it contains (plan_kind_set);
+// ev_start / ev_stop (may be null) are recorded around the fused kernel alone.
 NllLaunchInfo launch_nll(const DevPlan& plan, const ColPtrs& cols, long long n,
                          const double* d_consts, int P, void* scratch, SumPair* d_out,
-                         unsigned long long* d_bad, cudaStream_t stream, bool full,
+                         unsigned long long* d_bad, cudaStream_t stream, int ks,
                          cudaEvent_t ev_start = nullptr, cudaEvent_t ev_stop = nullptr);
 
-// True when the plan uses ChiSquare / JohnsonSU, or an ArgusBG point has p != 1/2
-// or |c| > 700 (host_consts: the P constant rows about to be launched).
-bool plan_needs_full(const DevPlan& plan, const double* host_consts, int P);
+// The smallest kernel build that covers the plan: 0 = Gaussian / Exponential /
+// ArgusBG (p = 1/2, |c| <= 700), 1 = + Chebychev / Polynomial, 2 = everything
+// (ChiSquare, JohnsonSU, general ArgusBG).  host_consts: the P rows about to launch.
+int plan_kind_set(const DevPlan& plan, const double* host_consts, int P);
 
 // Per-event values of the plan for one point (probabilities() when the plan is
 // normalised, PdfSpec::eval_batch when not).

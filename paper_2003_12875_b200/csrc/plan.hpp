@@ -31,7 +31,10 @@ enum LeafKind : int {
   LK_POLY = 6,     // c: [coef, a1..an]
 };
 
-enum TermFlags : int { TF_END_SUM = 1, TF_END_PROD = 2 };
+// END_* close the innermost sum / product after this term; BEGIN_SUM marks the
+// first term of a sum, BEGIN_PROD the term that closes the first sum (factor) of a
+// product (both set by compile_plan from the END flags).
+enum TermFlags : int { TF_END_SUM = 1, TF_END_PROD = 2, TF_BEGIN_SUM = 4, TF_BEGIN_PROD = 8 };
 
 struct DevTerm {
   int kind;   // LeafKind

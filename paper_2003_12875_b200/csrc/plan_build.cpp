@@ -182,9 +182,18 @@ HostPlan compile_plan(const Model& m, int pdf, bool normalized) {
   hp.dev.ncols = static_cast<int>(e.col_obs.size());
   hp.dev.stride = static_cast<int>(e.consts.size());
   int ends = 0;
+  bool first_factor = true;
   for (std::size_t i = 0; i < e.terms.size(); ++i) {
     hp.dev.t[i] = e.terms[i];
-    if (e.terms[i].flags) ++ends;
+    const int f = e.terms[i].flags;
+    if (f) ++ends;
+    const int prev = i == 0 ? (TF_END_SUM | TF_END_PROD) : e.terms[i - 1].flags;
+    if (prev & TF_END_SUM) hp.dev.t[i].flags |= TF_BEGIN_SUM;  // first term of a sum
+    if (f & TF_END_SUM) {
+      if (first_factor) hp.dev.t[i].flags |= TF_BEGIN_PROD;  // closes a product's first factor
+      first_factor = false;
+    }
+    if (f & TF_END_PROD) first_factor = true;
   }
   hp.dev.simple = ends == 1 ? 1 : 0;
   return hp;

@@ -411,7 +411,7 @@ def math_probe(which: str, x) -> np.ndarray:
     """The fused kernel's device exp ("exp") or log ("log") over an array (test hook)."""
     x = _f64(x)
     out = np.empty_like(x)
-    _check(lib().ffcu_math_probe({"exp": 0, "log": 1}[which], _dp(x), _dp(out), len(x)))
+    _check(lib().ffcu_math_probe({"exp": 0, "log": 1, "sqrt": 2, "rsqrt_seed": 3}[which], _dp(x), _dp(out), len(x)))
     return out
 
 

@@ -17,8 +17,8 @@ def ulps(a, b):
 
 def test_exp_accuracy_over_the_working_range():
     rng = np.random.default_rng(0)
-    # the kernel's exp is exact-to-2-ulp on |x| <= 707.7 and saturates beyond (fastmath.cuh)
-    x = np.concatenate([rng.uniform(-707.6, 707.6, 2_000_000), rng.uniform(-1, 1, 500_000),
+    # the kernel's exp is exact-to-2-ulp on |x| <= 707 and saturates beyond (fastmath.cuh)
+    x = np.concatenate([rng.uniform(-707.0, 707.0, 2_000_000), rng.uniform(-1, 1, 500_000),
                         rng.uniform(-40, 0, 500_000), np.array([0.0, -0.0, 1e-300, -1e-300, 1.0, -1.0])])
     got = fb.ffit.math_probe("exp", x)
     want = np.exp(x)
@@ -27,10 +27,10 @@ def test_exp_accuracy_over_the_working_range():
 
 
 def test_exp_saturation():
-    """Beyond |x| = 707.7 the kernel's exp saturates (0 below, +inf above); NaN / inf
+    """Beyond |x| = 707 the kernel's exp saturates (0 below, +inf above); NaN / inf
     arguments are never evaluated: events with non-finite data are flagged invalid by the
     kernels and non-finite parameters are rejected on the host."""
-    x = np.array([-800.0, -746.0, -707.8, 707.8, 710.0, 800.0, 1e300, -1e300])
+    x = np.array([-800.0, -746.0, -707.1, 707.1, 710.0, 800.0, 1e300, -1e300])
     got = fb.ffit.math_probe("exp", x)
     assert list(got[[0, 1, 2, 7]]) == [0.0, 0.0, 0.0, 0.0]
     assert np.all(np.isinf(got[[3, 4, 5, 6]]))
@@ -45,6 +45,19 @@ def test_log_accuracy_absolute_and_relative():
     err = np.abs(got - want)
     assert np.all(err <= np.maximum(2.0 * np.spacing(np.abs(want)), 2.3e-16))
     assert got[-6] == 0.0  # log(1) exactly
+
+
+def test_sqrt_unit_accuracy():
+    """ArgusBG's branch-free sqrt on (0, 1]: within 1 ulp of the IEEE sqrt."""
+    rng = np.random.default_rng(2)
+    t = np.concatenate([rng.uniform(0, 1, 1_000_000), 10.0 ** rng.uniform(-16, 0, 1_000_000),
+                        np.array([1.0, 0.25, 2.0 ** -52])])
+    got = fb.ffit.math_probe("sqrt", t)
+    assert np.max(ulps(got, np.sqrt(t))) <= 1.0
+    seed = fb.ffit.math_probe("rsqrt_seed", t)
+    rel = np.max(np.abs(seed * np.sqrt(t) - 1.0))
+    print(f"MUFU rsqrt seed max relative error: {rel:.3e}")
+    assert rel < 1e-4
 
 
 def test_log_subnormals():

@@ -164,6 +164,22 @@ def test_invalid_events_report_first_index():
     assert math.isinf(v.value) and v.first_invalid == 4321
 
 
+@pytest.mark.parametrize("kind", ["Chebychev", "Polynomial"])
+@pytest.mark.parametrize("order", [0, 1, 2, 3, 4, 5, 7])
+def test_polynomial_orders(kind, order):
+    """Compile-time orders 1-4 and the run-time loop (0, >4) agree with the oracle."""
+    coefs = [0.13, -0.07, 0.05, -0.03, 0.02, -0.011, 0.006][:order]
+    params = "".join(f"parameter a{i} {a} -1 1\n" for i, a in enumerate(coefs))
+    args = "".join(f", a{i}" for i in range(order))
+    text = f"observable z -1 1\n{params}pdf q {kind}(z{args})\n"
+    m = fb.Model.from_string(text)
+    o = OracleModel(text)
+    z = np.random.default_rng(order).uniform(-1, 1, 30000)
+    ds = fb.DataSet.from_columns({"z": z})
+    assert rel(fb.probabilities(m, ds), o.probabilities([z])) <= PER_EVENT
+    assert abs(fb.nll(m, ds).value - o.nll([z])[1]) <= NLL_TOL * abs(o.nll([z])[1])
+
+
 @pytest.mark.parametrize("p,c", [(0.7, -20.0), (0.5, -800.0), (0.5, 3.0), (1.3, 750.0)])
 def test_argus_general_path(p, c):
     """ArgusBG off the fast domain (p != 1/2 or |c| > 700) runs the full kernel build
@@ -255,6 +271,40 @@ pdf model AddPdf(sig, f, bkg)
     rng = np.random.default_rng(2)
     cols = [rng.uniform(-5, 5, 40_000), rng.uniform(0, 10, 40_000)]
     ds = fb.DataSet.from_columns({"x": cols[0], "y": cols[1]})
+    assert rel(fb.probabilities(m, ds), o.probabilities(cols)) <= PER_EVENT
+    assert abs(fb.nll(m, ds).value - o.nll(cols)[1]) <= NLL_TOL * abs(o.nll(cols)[1])
+
+
+def test_product_whose_first_factor_is_a_sum():
+    """ProdPdf(AddPdf(a, f, b) on x, Gaussian on y, AddPdf on z): multi-term sums as the
+    first and the last factor of a product."""
+    text = """
+observable x -5 5
+observable y -3 3
+observable z 0 4
+parameter m 0.3 -1 1
+parameter s 0.9 0.1 3
+parameter c -0.4 -2 2
+parameter f 0.35 0 1
+parameter my 0.1 -1 1
+parameter sy 1.2 0.1 3
+parameter cz -0.7 -2 2
+parameter a1 0.2 -1 1
+parameter g 0.5 0 1
+pdf gx Gaussian(x, m, s)
+pdf ex Exponential(x, c)
+pdf xmix AddPdf(gx, f, ex)
+pdf gy Gaussian(y, my, sy)
+pdf ez Exponential(z, cz)
+pdf pz Polynomial(z, a1)
+pdf zmix AddPdf(ez, g, pz)
+pdf model ProdPdf(xmix, gy, zmix)
+"""
+    m = fb.Model.from_string(text)
+    o = OracleModel(text)
+    rng = np.random.default_rng(8)
+    cols = [rng.uniform(-5, 5, 30000), rng.uniform(-3, 3, 30000), rng.uniform(0, 4, 30000)]
+    ds = fb.DataSet.from_columns({"x": cols[0], "y": cols[1], "z": cols[2]})
     assert rel(fb.probabilities(m, ds), o.probabilities(cols)) <= PER_EVENT
     assert abs(fb.nll(m, ds).value - o.nll(cols)[1]) <= NLL_TOL * abs(o.nll(cols)[1])
 

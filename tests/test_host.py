@@ -92,16 +92,18 @@ def test_set_param_range_and_constant():
 
 
 def test_plan_structure():
+    # flags: 1 END_SUM, 2 END_PROD, 4 BEGIN_SUM, 8 BEGIN_PROD
     kinds = {"GAUSS": 0, "EXPO": 1, "ARGUS": 4, "CHEB": 5}
     t, nc, st = fb.Model.from_string(configs.C1.text).plan()
-    assert [(x["kind"], x["flags"]) for x in t] == [(kinds["GAUSS"], 3)] and nc == 1 and st == 3
+    assert [(x["kind"], x["flags"]) for x in t] == [(kinds["GAUSS"], 15)] and nc == 1 and st == 3
     t, nc, st = fb.Model.from_string(configs.C2.text).plan()
-    assert [(x["kind"], x["flags"]) for x in t] == [(0, 0), (4, 3)] and nc == 1
+    assert [(x["kind"], x["flags"]) for x in t] == [(0, 4), (4, 11)] and nc == 1
     t, nc, st = fb.Model.from_string(configs.C3.text).plan()
-    assert [(x["kind"], x["col"], x["flags"]) for x in t] == [(0, 0, 1), (1, 1, 1), (5, 2, 3)] and nc == 3
+    assert [(x["kind"], x["col"], x["flags"]) for x in t] == [(0, 0, 13), (1, 1, 5), (5, 2, 7)] and nc == 3
     assert t[2]["order"] == 3
     t, nc, st = fb.Model.from_string(configs.C4.text).plan()
-    assert len(t) == 6 and t[-1]["flags"] == 3 and all(x["flags"] == 0 for x in t[:-1])
+    assert len(t) == 6 and t[-1]["flags"] == 11 and t[0]["flags"] == 4
+    assert all(x["flags"] == 0 for x in t[1:-1])
 
 
 def test_sum_of_products_plan():
@@ -123,7 +125,7 @@ pdf model AddPdf(sig, f, bkg)
 """
     m = fb.Model.from_string(text)
     t, nc, _ = m.plan()
-    assert [x["flags"] for x in t] == [1, 3, 1, 3] and nc == 2
+    assert [x["flags"] for x in t] == [13, 7, 13, 7] and nc == 2
     o = OracleModel(text)
     assert fb.normalization(m) == o.normalization()
 
