@@ -341,6 +341,59 @@ def run_reference(args, w):
     print(json.dumps(line), flush=True)
 
 
+def run_fit(args, w):
+    """BASELINE configs[4]: the Minuit-style fit loop (BFGS on central differences,
+    2d+1 points per launch, Hessian points in one launch) on one GPU; value = event-points/s
+    through the whole fit, plus NLL evaluations/s, fit wall time and the fitted parameters."""
+    import numpy as np
+    import torch
+
+    import paper_2003_12875_b200 as fb
+
+    rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    if rank != 0:
+        return
+    torch.cuda.set_device(local)
+    n = args.events or w.n_events
+    truth = fb.Model.from_string(w.text)
+    t0 = time.perf_counter()
+    cols, _ = fb.sample_host(truth, n, w.data_seed)
+    t_gen = time.perf_counter() - t0
+    ds = fb.DataSet.from_columns(cols)
+    model = fb.Model.from_string(w.text)
+    start = w.points(model, n_points=1, seed=w.point_seed)[0]
+    for name, v in zip(model.param_names, start):
+        if not model.is_constant(name):
+            model.set(name, v)
+    fb.nll_points(model, ds, start[None, :])  # warm-up (module load, first launch)
+    torch.cuda.synchronize()
+    fb.kernel_timer(True)
+    fb.kernel_timer_read()
+    launches0 = fb.kernel_launches()
+    r = fb.fit_gradient(model, ds, tolerance=1e-12, max_iterations=args.iterations)
+    torch.cuda.synchronize()
+    kms, kcount = fb.kernel_timer_read()
+    launches = fb.kernel_launches() - launches0
+    d = sum(1 for p in model.param_names if not model.is_constant(p))
+    line = {
+        "metric": METRIC, "value": r.n_nll_calls * n / r.wall_seconds, "unit": UNIT, "n_gpus": 1,
+        "steps": r.iterations, "warmup": 1, "ms_per_step": 1e3 * r.wall_seconds / max(r.n_launches, 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator, reference Rng)",
+        "config": {"workload": w.name, "description": w.description, "events_per_gpu": n,
+                   "points_per_launch": 2 * d + 1, "free_parameters": d},
+        "fit": {"converged": r.converged, "iterations": r.iterations, "launches": r.n_launches,
+                "nll_evaluations": r.n_nll_calls, "nll_evaluations_per_s": r.n_nll_calls / r.wall_seconds,
+                "wall_seconds": r.wall_seconds, "kernel_ms_total": kms, "kernel_launches_timed": kcount,
+                "nll_min": r.nll_min,
+                "parameters": {p.name: [p.value, p.uncertainty] for p in r.parameters},
+                "truth": dict(zip(truth.param_names, [float(v) for v in truth.theta()])),
+                "data_generation_s": t_gen},
+        "gpu_launches": int(launches),
+    }
+    print(json.dumps(line), flush=True)
+
+
 def _ref_param_names(text):
     out = []
     for line in (text or "").splitlines():
@@ -371,6 +424,8 @@ def main():
     ap.add_argument("--events", type=int, default=0, help="override events per GPU")
     ap.add_argument("--points", type=int, default=None, help="override points per launch")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--fit", action="store_true", help="time the Minuit-style fit loop (config 5 style)")
+    ap.add_argument("--iterations", type=int, default=50, help="fit iterations (--fit / c5)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
@@ -381,6 +436,8 @@ def main():
         w = configs.BY_INDEX[int(args.workload.lstrip("c")) - 1]
     if args.impl == "reference":
         run_reference(args, w)
+    elif args.fit or w is configs.C5:
+        run_fit(args, w)
     else:
         run_ours(args, w)
 
