@@ -36,6 +36,26 @@ def env_int(k, d):
     return int(os.environ.get(k, d))
 
 
+# The JSON line goes to the ORIGINAL stdout; everything else that writes to fd 1
+# (NCCL's version banner, library chatter) is redirected to stderr, so rank 0's
+# stdout carries exactly one line.
+_JSON_OUT = None
+
+
+def _claim_stdout():
+    global _JSON_OUT
+    if _JSON_OUT is None:
+        sys.stdout.flush()
+        _JSON_OUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
+
+
+def emit(line):
+    _claim_stdout()
+    _JSON_OUT.write(json.dumps(line) + "\n")
+    _JSON_OUT.flush()
+
+
 # ---------------------------------------------------------------------------
 # clocks during the timed region (B200_PROFILING.md recipe)
 
@@ -147,8 +167,14 @@ def run_ours(args, w):
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    # the exchange step (NCCL all-gather + fixed-order combine) runs whenever there is
+    # more than one rank; --force-collective runs it at N = 1 too (exercises the path)
+    coll = world > 1 or args.force_collective
+    if coll:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(world))
         dist.init_process_group("nccl", device_id=dev)
 
     model = fb.Model.from_string(w.text)
@@ -169,7 +195,7 @@ def run_ours(args, w):
     def step():
         with torch.cuda.stream(stream):
             fb.nll_points_device(model, ds, pts, d_sc.data_ptr(), d_bad.data_ptr(), stream.cuda_stream)
-            if world > 1:
+            if coll:
                 dist.all_gather_into_tensor(gathered.view(world * P, 2), d_sc)
                 fb.ffit.combine_pairs_device(gathered.data_ptr(), world, P, final.data_ptr(),
                                              stream.cuda_stream)
@@ -187,7 +213,7 @@ def run_ours(args, w):
     fb.kernel_timer_read()
     launches0 = fb.kernel_launches()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    if world > 1:
+    if coll:
         dist.barrier()
     torch.cuda.synchronize()
     for a, b in evs:
@@ -197,7 +223,7 @@ def run_ours(args, w):
         step()
         b.record(stream)
     torch.cuda.synchronize()
-    if world > 1:
+    if coll:
         dist.barrier()
     launches = fb.kernel_launches() - launches0
     kms, kcount = fb.kernel_timer_read()
@@ -206,38 +232,38 @@ def run_ours(args, w):
     step_ms = [a.elapsed_time(b) for a, b in evs]
     total_ms = sum(step_ms)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if world > 1:
+    if coll:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
     value = world * n * P * args.steps / (total_ms / 1e3)
 
     # sanity of the result (finite, no invalid event)
-    res = (final if world > 1 else d_sc).cpu().numpy()
+    res = (final if coll else d_sc).cpu().numpy()
     ok = bool(np.all(np.isfinite(res)) and int((d_bad.cpu().numpy() != -1).sum()) == 0)
 
     # --- end-to-end through the C ABI with host buffers (H2D + launch + D2H per step)
     pinned = {k: torch.from_numpy(cols[k]).pin_memory() for k in names}
     host_ptr_cols = {k: pinned[k].numpy() for k in names}
     e2e_steps = max(3, min(args.steps, 20))
-    if world > 1:
+    if coll:
         dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         ds.copy_from_host(host_ptr_cols)
         step()
-        host_res = (final if world > 1 else d_sc).cpu()
+        host_res = (final if coll else d_sc).cpu()
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
     t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-    if world > 1:
+    if coll:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_s = float(t.item())
     e2e = {"value": world * n * P * e2e_steps / e2e_s, "unit": UNIT,
            "h2d_bytes_per_step": int(n * 8 * len(names) + P * model.plan()[2] * 8),
            "d2h_bytes_per_step": int(host_res.numel() * 8),
            "path": "ffcu_dataset_copy_from_host (pinned) + ffcu_nll_points_device"
-                   + (" + NCCL all_gather + combine" if world > 1 else "") + " + D2H of the P results"}
+                   + (" + NCCL all_gather + combine" if coll else "") + " + D2H of the P results"}
 
     avg_kernel_ms = kms / max(kcount, 1)
     instr = w.fp64_instr_per_event_point * n * P
@@ -263,7 +289,7 @@ def run_ours(args, w):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, reference Rng)",
         "config": {"workload": w.name, "description": w.description, "events_per_gpu": n, "points_per_launch": P,
                    "l2": "flushed between timed steps (512 MiB write)",
-                   "parallelism": f"event shards x{world}" + (", NCCL all_gather of 2P doubles" if world > 1 else ""),
+                   "parallelism": f"event shards x{world}" + (", NCCL all_gather of 2P doubles" if coll else ""),
                    "launch": info},
         "roofline": roofline, "e2e": e2e, "clocks": clk, "gpu_launches": int(launches),
         "result_finite": ok,
@@ -271,8 +297,8 @@ def run_ours(args, w):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_port(w, [cols[k] for k in names], pts, n)
     if rank == 0:
-        print(json.dumps(line), flush=True)
-    if world > 1:
+        emit(line)
+    if coll:
         dist.destroy_process_group()
 
 
@@ -338,7 +364,7 @@ def run_reference(args, w):
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def run_fit(args, w):
@@ -391,7 +417,7 @@ def run_fit(args, w):
                 "data_generation_s": t_gen},
         "gpu_launches": int(launches),
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def _ref_param_names(text):
@@ -415,6 +441,7 @@ def _points_for_reference(w, o, n_points):
 
 
 def main():
+    _claim_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
@@ -425,6 +452,8 @@ def main():
     ap.add_argument("--points", type=int, default=None, help="override points per launch")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--fit", action="store_true", help="time the Minuit-style fit loop (config 5 style)")
+    ap.add_argument("--force-collective", action="store_true",
+                    help="run the NCCL all-gather + combine exchange even at N = 1")
     ap.add_argument("--iterations", type=int, default=50, help="fit iterations (--fit / c5)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
