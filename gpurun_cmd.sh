@@ -1,3 +1,8 @@
-python bench.py --force-collective --steps 10 --no-cpu-baseline > gpurun_out/bench_coll.json 2> gpurun_out/bench_coll.err; echo "coll rc=$?"
-python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29555 bench.py --gpus 1 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_torchrun.json 2> gpurun_out/bench_torchrun.err; echo "torchrun rc=$?"
-python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29556 bench.py --impl reference --gpus 1 --steps 2 --warmup 1 > gpurun_out/bench_torchrun_ref.json 2> gpurun_out/bench_torchrun_ref.err; echo "torchrun ref rc=$?"
+python -m pytest tests -m gpu -q --timeout 900 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+for w in c2 c1 c4 c3; do
+  python bench.py --workload $w --no-cpu-baseline --steps 20 > gpurun_out/sweep_${w}_v0.json 2>> gpurun_out/bench_err.log
+done
+python bench.py --steps 1 --warmup 3 --no-cpu-baseline --points 50 > gpurun_out/plain2.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:nll_kernel -s 3 -c 1 -o gpurun_out/prof_c2_v8 python bench.py --steps 1 --warmup 3 --no-cpu-baseline --points 50 > gpurun_out/ncu_full.log 2>&1
+echo done

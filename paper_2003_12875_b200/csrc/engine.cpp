@@ -229,7 +229,7 @@ void Engine::bind_columns(const HostPlan& plan, const DeviceDataset& ds, ColPtrs
 }
 
 const double* Engine::upload_constants(const HostPlan& plan, const double* thetas, int P,
-                                       cudaStream_t s) {
+                                       cudaStream_t s, double extra_scale) {
   const int k = slot_ ^= 1;
   // slot k fed the copy two calls ago; that copy must be done before reuse
   cuda_check(cudaEventSynchronize(staged_[k]), "cudaEventSynchronize");
@@ -237,7 +237,7 @@ const double* Engine::upload_constants(const HostPlan& plan, const double* theta
   const int stride = plan.dev.stride;
   for (int p = 0; p < P; ++p) {
     build_constants(plan, m_, thetas + static_cast<std::size_t>(p) * npar,
-                    h_consts_[k] + static_cast<std::size_t>(p) * stride);
+                    h_consts_[k] + static_cast<std::size_t>(p) * stride, extra_scale);
   }
   cuda_check(cudaMemcpyAsync(d_consts_[k], h_consts_[k],
                              static_cast<std::size_t>(P) * stride * sizeof(double),
@@ -263,7 +263,8 @@ int Engine::nll_points_device(const DeviceDataset& ds, const double* thetas, int
     cudaStreamWaitEvent(s, ev, 0);
     cudaEventDestroy(ev);
   }
-  const double* d_consts = upload_constants(plan_, thetas, P, s);
+  // the likelihood kernel evaluates p * 2^kPScaleLog2 (plan.hpp)
+  const double* d_consts = upload_constants(plan_, thetas, P, s, std::ldexp(1.0, kPScaleLog2));
   int launches = 0;
   if (ds.n == 0) {
     cuda_check(cudaMemsetAsync(d_pairs, 0, P * sizeof(SumPair), s), "cudaMemsetAsync");

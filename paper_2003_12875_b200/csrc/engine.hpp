@@ -95,7 +95,8 @@ class Engine {
  private:
   void bind_columns(const HostPlan& plan, const DeviceDataset& ds, ColPtrs& cols) const;
   void ensure(int device, int P, std::size_t scratch);
-  const double* upload_constants(const HostPlan& plan, const double* thetas, int P, cudaStream_t s);
+  const double* upload_constants(const HostPlan& plan, const double* thetas, int P, cudaStream_t s,
+                                 double extra_scale = 1.0);
 
   const Model& m_;
   HostPlan plan_;

@@ -18,6 +18,11 @@
 namespace ffb {
 
 constexpr int kMaxTerms = 32;
+// The likelihood kernel evaluates p * 2^kPScaleLog2 (folded into the coefficients
+// by build_constants): every positive p down to the smallest subnormal is then a
+// normal double, so the device log needs no subnormal path; the scale is taken
+// back out of the exponent exactly.
+constexpr int kPScaleLog2 = 54;
 constexpr int kMaxCols = 8;
 constexpr int kMaxOrder = 12;
 

@@ -199,7 +199,8 @@ HostPlan compile_plan(const Model& m, int pdf, bool normalized) {
   return hp;
 }
 
-void build_constants(const HostPlan& plan, const Model& m, const double* theta, double* row) {
+void build_constants(const HostPlan& plan, const Model& m, const double* theta, double* row,
+                     double extra_scale) {
   for (std::size_t i = 0; i < m.params.size(); ++i) {
     // the device exp assumes finite arguments (fastmath.cuh); the reference's
     // set_value range check excludes NaN / inf the same way (proj/src/graph.cpp:121)
@@ -208,7 +209,8 @@ void build_constants(const HostPlan& plan, const Model& m, const double* theta, 
     }
   }
   m.check_params(plan.pdf, theta);
-  const double scale = plan.normalized ? 1.0 / m.normalization(plan.pdf, theta) : 1.0;
+  const double scale =
+      (plan.normalized ? 1.0 / m.normalization(plan.pdf, theta) : 1.0) * extra_scale;
   Emitter e{m, theta, {}, {}, {}};
   e.root(plan.pdf, scale);
   if (static_cast<int>(e.consts.size()) != plan.dev.stride) usage_error("internal: plan drift");

@@ -24,6 +24,9 @@ HostPlan compile_plan(const Model& m, int pdf, bool normalized);
 // Writes one row of `plan.dev.stride` constants for parameter vector theta
 // (all model parameters, declaration order).  Validates the point first
 // (check_params, proj/src/pdfs.cpp:127-176) and computes every normalisation.
-void build_constants(const HostPlan& plan, const Model& m, const double* theta, double* row);
+// `extra_scale` multiplies the whole density (the likelihood kernel passes
+// 2^kPScaleLog2, see plan.hpp; exact, a power of two).
+void build_constants(const HostPlan& plan, const Model& m, const double* theta, double* row,
+                     double extra_scale = 1.0);
 
 }  // namespace ffb
