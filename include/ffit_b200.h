@@ -142,6 +142,24 @@ int ffcu_nll_points_partial(ffit_model* m, const ffit_dataset* ds, const double*
 int ffcu_nll_points_device(ffit_model* m, const ffit_dataset* ds, const double* points, int P,
                            double* d_sc, unsigned long long* d_bad, void* stream,
                            unsigned long long* n_evaluations);
+/* NLL and its analytic gradient in ONE fused pass over the events (SURVEY.md
+ * §8(f) f1; replaces the finite-difference gradients a Minuit-style driver builds
+ * from 2d+1 proj/src/eval.cpp:119-163 evaluations).  grads: P x param_count,
+ * dNLL/dtheta_j in ffit_model_param_name order, 0 for constant parameters, NaN
+ * where values[p] is +inf.  FFIT_ERR_USAGE if the model's gradient layout exceeds
+ * the device pass (more than 48 accumulators). */
+int ffcu_nll_grad(ffit_model* m, const ffit_dataset* ds, const double* points, int P,
+                  double* values, double* grads, long long* first_invalid,
+                  unsigned long long* n_evaluations);
+/* Accumulators per point of the gradient pass (slot 0 = the event NLL sum). */
+int ffcu_grad_slot_count(ffit_model* m, int* nslots);
+/* Multi-GPU split of ffcu_nll_grad: the per-shard uncombined Neumaier pairs
+ * (sc: P x nslots x 2), then the host finish from the rank-combined slot sums
+ * (P x nslots) with the global event count. */
+int ffcu_nll_grad_partial(ffit_model* m, const ffit_dataset* ds, const double* points, int P,
+                          double* sc, long long* first_invalid, unsigned long long* n_evaluations);
+int ffcu_nll_grad_finish(ffit_model* m, const double* points, int P, const double* slot_sums,
+                         double n_events, double* values, double* grads);
 /* Fixed-rank-order compensated combine of R x P device pairs into P pairs. */
 int ffcu_combine_pairs_device(const double* d_in, int R, int P, double* d_out, void* stream);
 /* Extended term nu - N log nu per point (0 for non-extended models). */
@@ -163,6 +181,9 @@ int ffcu_plan_info(const ffit_model* m, int* nterms, int* ncols, int* stride);
 int ffcu_plan_term(const ffit_model* m, int i, int* kind, int* col, int* order, int* flags,
                    int* coff);
 int ffcu_point_constants(const ffit_model* m, const double* point, double* row);
+/* d coef_c / d theta_param for each plan term c (the row's coefficient entries;
+ * host logic of the gradient pass, no GPU needed). */
+int ffcu_coef_derivatives(const ffit_model* m, const double* point, int param, double* out);
 int ffcu_model_pdf_count(const ffit_model* m);
 const char* ffcu_model_pdf_name(const ffit_model* m, int i);
 int ffcu_model_observable_count(const ffit_model* m);
@@ -172,6 +193,12 @@ const char* ffcu_model_observable_name(const ffit_model* m, int i);
  * launch per iteration; Hessian uncertainties from one launch. */
 int ffcu_fit_gradient(ffit_model* m, const ffit_dataset* ds, double tolerance,
                       long max_iterations, ffit_fit_result** out);
+/* analytic = 1: gradients from the fused NLL + gradient pass when the model's
+ * layout fits it (ffcu_fit_gradient's default), 0: central finite differences. */
+int ffcu_fit_gradient_opts(ffit_model* m, const ffit_dataset* ds, double tolerance,
+                           long max_iterations, int analytic, ffit_fit_result** out);
+/* 1 if the fit's gradients came from the fused pass. */
+int ffcu_result_analytic_gradient(const ffit_fit_result* r);
 int ffcu_result_iterations(const ffit_fit_result* r);
 unsigned long long ffcu_result_launches(const ffit_fit_result* r);
 int ffcu_result_trace(const ffit_fit_result* r, double* out, int cap);

@@ -70,6 +70,10 @@ SIGNATURES = {
     "ffcu_nll_points": (I, [VP, VP, DP, I, DP, LLP, ULLP]),
     "ffcu_nll_points_partial": (I, [VP, VP, DP, I, DP, LLP, ULLP]),
     "ffcu_nll_points_device": (I, [VP, VP, DP, I, VP, VP, VP, ULLP]),
+    "ffcu_nll_grad": (I, [VP, VP, DP, I, DP, DP, LLP, ULLP]),
+    "ffcu_grad_slot_count": (I, [VP, IP]),
+    "ffcu_nll_grad_partial": (I, [VP, VP, DP, I, DP, LLP, ULLP]),
+    "ffcu_nll_grad_finish": (I, [VP, DP, I, DP, D, DP, DP]),
     "ffcu_combine_pairs_device": (I, [VP, I, I, VP, VP]),
     "ffcu_extended_terms": (I, [VP, DP, I, D, DP]),
     "ffcu_probabilities_at": (I, [VP, VP, DP, DP]),
@@ -79,11 +83,14 @@ SIGNATURES = {
     "ffcu_plan_info": (I, [VP, IP, IP, IP]),
     "ffcu_plan_term": (I, [VP, I, IP, IP, IP, IP, IP]),
     "ffcu_point_constants": (I, [VP, DP, DP]),
+    "ffcu_coef_derivatives": (I, [VP, DP, I, DP]),
     "ffcu_model_pdf_count": (I, [VP]),
     "ffcu_model_pdf_name": (CP, [VP, I]),
     "ffcu_model_observable_count": (I, [VP]),
     "ffcu_model_observable_name": (CP, [VP, I]),
     "ffcu_fit_gradient": (I, [VP, VP, D, ctypes.c_long, ctypes.POINTER(VP)]),
+    "ffcu_fit_gradient_opts": (I, [VP, VP, D, ctypes.c_long, I, ctypes.POINTER(VP)]),
+    "ffcu_result_analytic_gradient": (I, [VP]),
     "ffcu_result_iterations": (I, [VP]),
     "ffcu_result_launches": (ULL, [VP]),
     "ffcu_result_trace": (I, [VP, DP, I]),

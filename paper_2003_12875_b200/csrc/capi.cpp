@@ -414,6 +414,75 @@ FFB_API int ffcu_nll_points_device(ffit_model* m, const ffit_dataset* ds, const 
   });
 }
 
+FFB_API int ffcu_grad_slot_count(ffit_model* m, int* nslots) {
+  return guarded([&] {
+    require(m, "model");
+    require(nslots, "nslots");
+    const ffb::GradPlan& gp = engine(m).grad_plan();
+    if (!gp.ok) ffb::usage_error("analytic gradient unavailable for this model: " + gp.why);
+    *nslots = gp.dev.nslots;
+  });
+}
+
+FFB_API int ffcu_nll_grad(ffit_model* m, const ffit_dataset* ds, const double* points, int P,
+                          double* values, double* grads, long long* first_invalid,
+                          unsigned long long* n_evaluations) {
+  return guarded([&] {
+    require(m, "model");
+    require(ds, "dataset");
+    require(points, "points");
+    require(values, "values");
+    require(grads, "grads");
+    if (P < 0) ffb::usage_error("P must be >= 0");
+    if (P == 0) {
+      if (n_evaluations) *n_evaluations = 0;
+      return;
+    }
+    const ffb::NllGradResult r = engine(m).nll_grad_points(*ds->d, points, P);
+    const std::size_t npar = m->m->params.size();
+    for (int p = 0; p < P; ++p) {
+      values[p] = r.value[p];
+      if (first_invalid) first_invalid[p] = r.first_invalid[p];
+    }
+    std::copy(r.grad.begin(), r.grad.begin() + static_cast<std::ptrdiff_t>(P * npar), grads);
+    if (n_evaluations) *n_evaluations = r.launches;
+  });
+}
+
+FFB_API int ffcu_nll_grad_partial(ffit_model* m, const ffit_dataset* ds, const double* points, int P,
+                                  double* sc, long long* first_invalid, unsigned long long* n_evaluations) {
+  return guarded([&] {
+    require(m, "model");
+    require(ds, "dataset");
+    require(points, "points");
+    require(sc, "sc");
+    if (P < 0) ffb::usage_error("P must be >= 0");
+    if (P == 0) return;
+    const ffb::NllGradResult r = engine(m).nll_grad_points(*ds->d, points, P);
+    for (std::size_t k = 0; k < r.slots.size(); ++k) {
+      sc[2 * k] = r.slots[k].s;
+      sc[2 * k + 1] = r.slots[k].c;
+    }
+    if (first_invalid) {
+      for (int p = 0; p < P; ++p) first_invalid[p] = r.first_invalid[p];
+    }
+    if (n_evaluations) *n_evaluations = r.launches;
+  });
+}
+
+FFB_API int ffcu_nll_grad_finish(ffit_model* m, const double* points, int P, const double* slot_sums,
+                                 double n_events, double* values, double* grads) {
+  return guarded([&] {
+    require(m, "model");
+    require(points, "points");
+    require(slot_sums, "slot_sums");
+    require(values, "values");
+    require(grads, "grads");
+    if (P < 0) ffb::usage_error("P must be >= 0");
+    engine(m).grad_finish(points, P, slot_sums, n_events, values, grads);
+  });
+}
+
 FFB_API int ffcu_combine_pairs_device(const double* d_in, int R, int P, double* d_out, void* stream) {
   return guarded([&] {
     require(d_in, "d_in");
@@ -503,6 +572,19 @@ FFB_API int ffcu_point_constants(const ffit_model* m, const double* point, doubl
     require(row, "row");
     const std::vector<double> th = point_or_current(*m->m, point);
     ffb::build_constants(m->engine->likelihood_plan(), *m->m, th.data(), row);
+  });
+}
+
+FFB_API int ffcu_coef_derivatives(const ffit_model* m, const double* point, int param, double* out) {
+  return guarded([&] {
+    require(m, "model");
+    require(out, "out");
+    if (param < 0 || param >= static_cast<int>(m->m->params.size())) ffb::usage_error("parameter index out of range");
+    const std::vector<double> th = point_or_current(*m->m, point);
+    const ffb::HostPlan& plan = m->engine->likelihood_plan();
+    m->m->check_params(plan.pdf, th.data());
+    const std::vector<double> d = ffb::coef_derivatives(plan, *m->m, th.data(), param, 1.0);
+    std::copy(d.begin(), d.end(), out);
   });
 }
 
@@ -629,12 +711,18 @@ FFB_API int ffit_fit(ffit_model* m, const ffit_dataset* ds, ffit_mode mode, doub
 
 FFB_API int ffcu_fit_gradient(ffit_model* m, const ffit_dataset* ds, double tolerance,
                               long max_iterations, ffit_fit_result** out) {
+  return ffcu_fit_gradient_opts(m, ds, tolerance, max_iterations, 1, out);
+}
+
+FFB_API int ffcu_fit_gradient_opts(ffit_model* m, const ffit_dataset* ds, double tolerance,
+                                   long max_iterations, int analytic, ffit_fit_result** out) {
   return guarded([&] {
     require(m, "model");
     require(ds, "dataset");
     require(out, "out");
     ffb::FitOptions o;
     o.record_trace = true;
+    o.analytic_gradient = analytic != 0;
     if (tolerance > 0.0) o.tolerance = tolerance;
     if (max_iterations > 0) o.max_iterations = static_cast<int>(max_iterations);
     auto r = std::make_unique<ffit_fit_result>();
@@ -644,6 +732,7 @@ FFB_API int ffcu_fit_gradient(ffit_model* m, const ffit_dataset* ds, double tole
 }
 
 FFB_API int ffit_result_converged(const ffit_fit_result* r) { return r->r.converged ? 1 : 0; }
+FFB_API int ffcu_result_analytic_gradient(const ffit_fit_result* r) { return r->r.analytic_gradient ? 1 : 0; }
 FFB_API double ffit_result_nll(const ffit_fit_result* r) { return r->r.nll_min; }
 FFB_API unsigned long long ffit_result_nll_calls(const ffit_fit_result* r) { return r->r.n_nll_calls; }
 FFB_API double ffit_result_wall_seconds(const ffit_fit_result* r) { return r->r.wall_seconds; }

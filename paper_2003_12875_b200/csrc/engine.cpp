@@ -1,5 +1,6 @@
 #include "engine.hpp"
 
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstring>
@@ -168,6 +169,8 @@ Engine::~Engine() {
     cudaFree(d_bad_);
     cudaFreeHost(h_pairs_);
     cudaFreeHost(h_bad_);
+    cudaFree(d_gslots_);
+    cudaFreeHost(h_gslots_);
     if (stream_) cudaStreamDestroy(stream_);
     cudaSetDevice(prev);
   }
@@ -324,6 +327,124 @@ NllResult Engine::nll_points(const DeviceDataset& ds, const double* thetas, int 
                        : (h_pairs_[i].s + h_pairs_[i].c) +
                              m_.extended_term(th + static_cast<std::size_t>(i) * npar,
                                               static_cast<double>(ds.n));
+    }
+  }
+  return r;
+}
+
+const GradPlan& Engine::grad_plan() {
+  std::vector<bool> cst(m_.params.size());
+  for (std::size_t i = 0; i < cst.size(); ++i) cst[i] = m_.params[i].constant;
+  if (grad_const_.empty() || cst != grad_const_) {
+    grad_ = compile_grad_plan(plan_, m_);
+    if (grad_.ok && !grad_layout_fits(plan_.dev, grad_.dev)) {
+      grad_.ok = false;
+      grad_.why = "gradient accumulators do not fit one CTA's shared memory";
+    }
+    grad_const_ = cst;
+  }
+  return grad_;
+}
+
+void Engine::grad_finish(const double* thetas, int P, const double* slot_sums, double n_events,
+                         double* values, double* grads) {
+  const GradPlan& gp = grad_plan();
+  if (!gp.ok) usage_error("analytic gradient unavailable for this model: " + gp.why);
+  const int npar = static_cast<int>(m_.params.size());
+  const int S = gp.dev.nslots;
+  const int nt = plan_.dev.nterms;
+  std::vector<double> dc;
+  for (int p = 0; p < P; ++p) {
+    const double* th = thetas + static_cast<std::size_t>(p) * npar;
+    const double* q = slot_sums + static_cast<std::size_t>(p) * S;
+    double* g = grads + static_cast<std::size_t>(p) * npar;
+    values[p] = q[0] + m_.extended_term(th, n_events);
+    for (int j = 0; j < npar; ++j) g[j] = 0.0;
+    m_.check_params(plan_.pdf, th);
+    for (int j = 0; j < npar; ++j) {
+      if (m_.params[j].constant) continue;
+      dc = coef_derivatives(plan_, m_, th, j, std::ldexp(1.0, kPScaleLog2));
+      double a = 0.0;
+      for (int i = 0; i < nt; ++i) a += q[gp.a_slot[i]] * dc[i];
+      g[j] = -a;
+    }
+    for (int k = 1; k < S; ++k) {
+      const int j = gp.slot_param[k];
+      if (j >= 0) g[j] -= q[k];
+    }
+    if (m_.extended()) {  // d(nu - N log nu)/d y_k = 1 - N / nu
+      double nu = 0.0;
+      for (const int k : m_.pdfs[m_.root].params) nu += th[k];
+      for (const int k : m_.pdfs[m_.root].params) {
+        if (!m_.params[k].constant) g[k] += 1.0 - n_events / nu;
+      }
+    }
+  }
+}
+
+NllGradResult Engine::nll_grad_points(const DeviceDataset& ds, const double* thetas, int P) {
+  const GradPlan& gp = grad_plan();
+  if (!gp.ok) usage_error("analytic gradient unavailable for this model: " + gp.why);
+  NllGradResult r;
+  const int npar = static_cast<int>(m_.params.size());
+  const int S = gp.dev.nslots;
+  r.nslots = S;
+  r.value.resize(P);
+  r.grad.resize(static_cast<std::size_t>(P) * npar);
+  r.first_invalid.resize(P);
+  r.slots.resize(static_cast<std::size_t>(P) * S);
+  DeviceGuard guard(ds.device);
+  std::vector<double> sums;
+  for (int p0 = 0; p0 < P; p0 += kMaxPointsPerLaunch) {
+    const int np = std::min(kMaxPointsPerLaunch, P - p0);
+    const double* th = thetas + static_cast<std::size_t>(p0) * npar;
+    const std::size_t scratch = ds.n > 0 ? nll_grad_scratch_bytes(ds.n, np, plan_.dev, gp.dev) : 0;
+    ensure(ds.device, np, scratch);
+    const std::size_t need = static_cast<std::size_t>(np) * S;
+    if (need > cap_gslots_) {
+      cuda_check(cudaStreamSynchronize(stream_), "cudaStreamSynchronize");
+      cudaFree(d_gslots_);
+      cudaFreeHost(h_gslots_);
+      cuda_check(cudaMalloc(&d_gslots_, need * sizeof(SumPair)), "cudaMalloc(gslots)");
+      cuda_check(cudaHostAlloc(&h_gslots_, need * sizeof(SumPair), cudaHostAllocDefault), "cudaHostAlloc");
+      cap_gslots_ = need;
+    }
+    const double* d_consts = upload_constants(plan_, th, np, stream_, std::ldexp(1.0, kPScaleLog2));
+    if (ds.n == 0) {
+      cuda_check(cudaMemsetAsync(d_gslots_, 0, need * sizeof(SumPair), stream_), "cudaMemsetAsync");
+      cuda_check(cudaMemsetAsync(d_bad_, 0xff, np * sizeof(unsigned long long), stream_), "cudaMemsetAsync");
+    } else {
+      ColPtrs cols;
+      bind_columns(plan_, ds, cols);
+      const int ks = plan_kind_set(plan_.dev, h_consts_[slot_], np);
+      const NllLaunchInfo li =
+          launch_nll_grad(plan_.dev, gp.dev, cols, ds.n, d_consts, np, d_scratch_, d_gslots_, d_bad_, stream_, ks);
+      cuda_check(cudaGetLastError(), "launch_nll_grad");
+      r.launches += li.launches;
+      count_launches(li.launches);
+    }
+    cuda_check(cudaMemcpyAsync(h_gslots_, d_gslots_, need * sizeof(SumPair), cudaMemcpyDeviceToHost, stream_),
+               "cudaMemcpyAsync(gslots)");
+    cuda_check(cudaMemcpyAsync(h_bad_, d_bad_, np * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream_),
+               "cudaMemcpyAsync(bad)");
+    cuda_check(cudaStreamSynchronize(stream_), "nll_grad kernels");
+    sums.resize(need);
+    for (std::size_t k = 0; k < need; ++k) {
+      r.slots[static_cast<std::size_t>(p0) * S + k] = h_gslots_[k];
+      sums[k] = h_gslots_[k].s + h_gslots_[k].c;
+    }
+    grad_finish(th, np, sums.data(), static_cast<double>(ds.n), r.value.data() + p0,
+                r.grad.data() + static_cast<std::size_t>(p0) * npar);
+    for (int i = 0; i < np; ++i) {
+      const int p = p0 + i;
+      const bool bad = h_bad_[i] != kNoInvalid;
+      r.first_invalid[p] = bad ? static_cast<long long>(h_bad_[i]) : -1;
+      if (bad) {
+        r.value[p] = std::numeric_limits<double>::infinity();
+        for (int j = 0; j < npar; ++j) {
+          r.grad[static_cast<std::size_t>(p) * npar + j] = std::numeric_limits<double>::quiet_NaN();
+        }
+      }
     }
   }
   return r;

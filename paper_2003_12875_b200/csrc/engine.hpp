@@ -63,6 +63,17 @@ struct NllResult {
   unsigned long long launches = 0;
 };
 
+// Fused NLL + gradient: value[p] as NllResult; grad[p * npar + j] = dNLL/dtheta_j
+// for the free parameters (0 for constant ones); NaN gradients with +inf values.
+struct NllGradResult {
+  std::vector<double> value;
+  std::vector<double> grad;
+  std::vector<long long> first_invalid;
+  unsigned long long launches = 0;
+  int nslots = 0;
+  std::vector<SumPair> slots;  // raw per-point accumulators (P x nslots, events only)
+};
+
 class Engine {
  public:
   explicit Engine(const Model& m);
@@ -78,6 +89,19 @@ class Engine {
   // constant upload are part of the call.  Returns kernels launched.
   int nll_points_device(const DeviceDataset& ds, const double* thetas, int P, SumPair* d_pairs,
                         unsigned long long* d_bad, cudaStream_t stream);
+
+  // Analytic gradient in the same pass over the events (plan.hpp DevGradPlan):
+  // P points, one launch pair per <= 512 points.  Throws Usage when the model's
+  // gradient layout does not fit the device pass (grad_plan().why).
+  NllGradResult nll_grad_points(const DeviceDataset& ds, const double* thetas, int P);
+
+  // Host finish of the gradient from the (rank-combined) slot sums: P x nslots
+  // values in `slot_sums`, n_events the global event count.
+  void grad_finish(const double* thetas, int P, const double* slot_sums, double n_events,
+                   double* values, double* grads);
+
+  // Current gradient layout (recompiled when parameters change constness).
+  const GradPlan& grad_plan();
 
   // probabilities() (proj/src/eval.cpp:174-192): normalised per-event values.
   void probabilities(const DeviceDataset& ds, const double* theta, double* out, bool out_on_device,
@@ -116,6 +140,11 @@ class Engine {
   SumPair* h_pairs_ = nullptr;             // pinned
   unsigned long long* h_bad_ = nullptr;    // pinned
   NllLaunchInfo last_{};
+  GradPlan grad_{};
+  std::vector<bool> grad_const_;  // constness the layout was compiled for
+  SumPair* d_gslots_ = nullptr;
+  SumPair* h_gslots_ = nullptr;  // pinned
+  std::size_t cap_gslots_ = 0;
 };
 
 // Optional per-launch timing of the fused NLL kernel (CUDA events on the

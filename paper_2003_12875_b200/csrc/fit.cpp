@@ -282,12 +282,77 @@ FitResult fit_nelder_mead(Model& m, Engine& e, const DeviceDataset& ds, const Fi
   return result;
 }
 
+namespace {
+
+// Value and u-space gradient at a batch of u points.  Analytic: the fused NLL +
+// gradient pass (one launch pair for all points), chain rule through the sine
+// transform d theta / d u = (hi - lo) cos(u) / 2.  Otherwise central differences:
+// 2d+1 NLL points per u point, one launch.
+struct GradObjective {
+  BatchObjective& f;
+  bool analytic;
+  double h;
+  std::vector<double> curv;  // finite differences: diagonal curvature at the first point
+
+  void operator()(const std::vector<std::vector<double>>& us, std::vector<double>& fv,
+                  std::vector<std::vector<double>>& gu) {
+    const std::size_t d = f.free_ids.size();
+    fv.assign(us.size(), 0.0);
+    gu.assign(us.size(), std::vector<double>(d, 0.0));
+    if (analytic) {
+      const std::size_t npar = f.m.params.size();
+      std::vector<double> rows(us.size() * npar);
+      for (std::size_t k = 0; k < us.size(); ++k) {
+        const std::vector<double> th = f.theta_of(us[k]);
+        std::copy(th.begin(), th.end(), rows.begin() + static_cast<std::ptrdiff_t>(k * npar));
+      }
+      const NllGradResult r = f.e.nll_grad_points(f.ds, rows.data(), static_cast<int>(us.size()));
+      f.calls += us.size();
+      f.batches += 1;
+      f.kernels += r.launches;
+      for (std::size_t k = 0; k < us.size(); ++k) {
+        fv[k] = r.value[k];
+        for (std::size_t i = 0; i < d; ++i) {
+          const Parameter& p = f.m.params[f.free_ids[i]];
+          gu[k][i] = r.grad[k * npar + f.free_ids[i]] * 0.5 * (p.hi - p.lo) * std::cos(us[k][i]);
+        }
+      }
+      return;
+    }
+    std::vector<std::vector<double>> pts;
+    for (const auto& u : us) {
+      pts.push_back(u);
+      for (std::size_t i = 0; i < d; ++i) {
+        std::vector<double> a = u, b = u;
+        a[i] += h;
+        b[i] -= h;
+        pts.push_back(a);
+        pts.push_back(b);
+      }
+    }
+    const std::vector<double> v = f(pts);
+    curv.assign(d, 0.0);
+    for (std::size_t k = 0; k < us.size(); ++k) {
+      const double* w = v.data() + k * (2 * d + 1);
+      fv[k] = w[0];
+      for (std::size_t i = 0; i < d; ++i) {
+        gu[k][i] = (w[1 + 2 * i] - w[2 + 2 * i]) / (2.0 * h);
+        if (k == 0) curv[i] = (w[1 + 2 * i] - 2.0 * w[0] + w[2 + 2 * i]) / (h * h);
+      }
+    }
+  }
+};
+
+}  // namespace
+
 FitResult fit_gradient(Model& m, Engine& e, const DeviceDataset& ds, const FitOptions& o) {
   const auto t0 = std::chrono::steady_clock::now();
   BatchObjective f{m, e, ds, m.free_parameters()};
   validate(m, o, f.free_ids);
   const std::size_t d = f.free_ids.size();
   const double h = o.fd_step;
+  const bool analytic = o.analytic_gradient && e.grad_plan().ok;
+  GradObjective fg{f, analytic, h, {}};
   std::vector<double> u = start_u(m, f.free_ids);
   std::vector<double> u_prev, g_prev, u_best = u;
   std::vector<std::vector<double>> H(d, std::vector<double>(d, 0.0));
@@ -295,38 +360,45 @@ FitResult fit_gradient(Model& m, Engine& e, const DeviceDataset& ds, const FitOp
   bool have_prev = false, converged = false;
   int backtracks = 0, iter = 0;
   FitResult result;
+  result.analytic_gradient = analytic;
+  std::vector<double> fv;
+  std::vector<std::vector<double>> gv;
   for (; iter < o.max_iterations; ++iter) {
-    // one launch: the centre and the 2d central-difference points
-    std::vector<std::vector<double>> pts(1, u);
-    for (std::size_t i = 0; i < d; ++i) {
-      std::vector<double> a = u, b = u;
-      a[i] += h;
-      b[i] -= h;
-      pts.push_back(a);
-      pts.push_back(b);
-    }
-    const std::vector<double> v = f(pts);
-    const double f0 = v[0];
-    if (!std::isfinite(f0) || (have_prev && f0 > f_prev)) {
-      if (!have_prev) numeric_error("NLL is not finite at the starting parameters (zero-probability entry)");
-      if (++backtracks > 40) break;
-      for (std::size_t i = 0; i < d; ++i) u[i] = u_prev[i] + 0.5 * (u[i] - u_prev[i]);
-      continue;
-    }
-    backtracks = 0;
-    if (o.record_trace) result.trace.push_back(f0);
-    if (f0 < f_best) {
-      f_best = f0;
-      u_best = u;
-    }
-    std::vector<double> g(d), curv(d);
-    for (std::size_t i = 0; i < d; ++i) {
-      g[i] = (v[1 + 2 * i] - v[2 + 2 * i]) / (2.0 * h);
-      curv[i] = (v[1 + 2 * i] - 2.0 * f0 + v[2 + 2 * i]) / (h * h);
-    }
+    std::vector<double> g;
+    double f0;
     if (!have_prev) {
-      for (std::size_t i = 0; i < d; ++i) H[i][i] = curv[i] > 0.0 ? 1.0 / curv[i] : 1e-2;
-    } else {  // BFGS update of the inverse Hessian
+      // start: the centre plus, for the initial inverse-Hessian diagonal, the
+      // gradient at u +- h e_i (analytic: one launch of 2d+1 points; finite
+      // differences: the curvature comes from the centre's own 2d+1 NLL values)
+      std::vector<std::vector<double>> us(1, u);
+      if (analytic) {
+        for (std::size_t i = 0; i < d; ++i) {
+          std::vector<double> a = u, b = u;
+          a[i] += h;
+          b[i] -= h;
+          us.push_back(a);
+          us.push_back(b);
+        }
+      }
+      fg(us, fv, gv);
+      f0 = fv[0];
+      if (!std::isfinite(f0)) numeric_error("NLL is not finite at the starting parameters (zero-probability entry)");
+      g = gv[0];
+      for (std::size_t i = 0; i < d; ++i) {
+        const double curv = analytic ? (gv[1 + 2 * i][i] - gv[2 + 2 * i][i]) / (2.0 * h) : fg.curv[i];
+        H[i][i] = curv > 0.0 ? 1.0 / curv : 1e-2;
+      }
+    } else {
+      fg({u}, fv, gv);
+      f0 = fv[0];
+      g = gv[0];
+      if (!std::isfinite(f0) || f0 > f_prev) {
+        if (++backtracks > 40) break;
+        for (std::size_t i = 0; i < d; ++i) u[i] = u_prev[i] + 0.5 * (u[i] - u_prev[i]);
+        continue;
+      }
+      backtracks = 0;
+      // BFGS update of the inverse Hessian
       std::vector<double> s(d), y(d);
       double sy = 0.0;
       for (std::size_t i = 0; i < d; ++i) {
@@ -348,6 +420,11 @@ FitResult fit_gradient(Model& m, Engine& e, const DeviceDataset& ds, const FitOp
           }
         }
       }
+    }
+    if (o.record_trace) result.trace.push_back(f0);
+    if (f0 < f_best) {
+      f_best = f0;
+      u_best = u;
     }
     double edm = 0.0;
     std::vector<double> step(d, 0.0);

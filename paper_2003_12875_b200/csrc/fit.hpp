@@ -4,8 +4,10 @@
 //    in sine-transformed space, central-difference Hessian) with every batch of
 //    independent points -- the initial simplex, a shrink, the 1+2d+2d(d-1) Hessian
 //    points -- issued as ONE multi-point launch.
-//  * fit_gradient: Minuit-style quasi-Newton (BFGS on central finite-difference
-//    gradients); each iteration is one launch of 2d+1 points.
+//  * fit_gradient: Minuit-style quasi-Newton (BFGS).  Gradients from the fused NLL +
+//    gradient pass (one point per iteration) when the model's
+//    layout fits it, else central finite differences (one launch of 2d+1 points per
+//    iteration).
 #pragma once
 
 #include <string>
@@ -20,6 +22,7 @@ struct FitOptions {
   int max_iterations = 10000;
   bool record_trace = false;
   double fd_step = 1e-4;    // u-space step for gradients / Hessian
+  bool analytic_gradient = true;  // fit_gradient: the fused NLL + gradient pass when available
 };
 
 struct FittedParameter {
@@ -38,6 +41,7 @@ struct FitResult {
   int iterations = 0;
   double wall_seconds = 0.0;
   bool uncertainties_valid = true;
+  bool analytic_gradient = false;  // fit_gradient used the fused gradient pass
   std::vector<double> trace;
 };
 

@@ -96,6 +96,13 @@ class Model {
   // PdfSpec::max_hint: 1024-point grid max * 1.1 (proj/src/pdfs.cpp:309-323).
   double max_hint(int pdf, const double* theta) const;
 
+  // Parameter derivatives for the fused gradient pass (model_grad.cpp): of the sum
+  // coefficients, of a normalisation, of a 1-D subtree's unnormalised density.
+  bool depends_on(int pdf, int param) const;
+  std::vector<double> fractions_grad(int pdf, const double* theta, int param) const;
+  double normalization_grad(int pdf, const double* theta, int param) const;
+  double eval_unnorm_1d_grad(int pdf, const double* theta, double x, int param) const;
+
   // Extended term nu - N log nu (0 for non-extended models).
   double extended_term(const double* theta, double n_events) const;
 

@@ -57,4 +57,30 @@ struct DevPlan {
   DevTerm t[kMaxTerms];
 };
 
+// Fused NLL + gradient pass (kernels.cu nll_grad_kernel).  With W_f(x) = the product
+// of the OTHER factors of term c's product divided by p (1/p for a single sum), the
+// kernel sums per point and tile:
+//   slot 0            sum -log p
+//   slot g[c].slot    A_c = sum W_f leaf_c            (the host applies d coef_c / d theta)
+//   the next popcount(pmask) slots
+//                     B_cm = sum W_f coef_c d leaf_c / d phi_m, one per set bit m of
+//                     pmask in the leaf's parameter order (Gaussian mu, sigma; ArgusBG
+//                     m0, c, p; JohnsonSU mu, lambda, gamma, delta; polynomial a_1..a_n)
+// so that dNLL/dtheta_j = -(sum_c A_c d coef_c/d theta_j + sum_{B_cm: phi_m = theta_j} B_cm).
+constexpr int kMaxGradSlots = 48;
+constexpr int kMaxFactors = 16;
+
+struct DevGradTerm {
+  int slot;     // A_c slot; the B slots follow
+  int pmask;    // leaf parameters differentiated on the device
+  int factor;   // factor (sum) this term belongs to, 0..nfactors-1
+  int fbeg, fend;  // factor range of the term's product
+};
+
+struct DevGradPlan {
+  int nslots;
+  int nfactors;
+  DevGradTerm g[kMaxTerms];
+};
+
 }  // namespace ffb

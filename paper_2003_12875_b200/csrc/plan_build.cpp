@@ -16,6 +16,7 @@ struct Emitter {
   std::vector<DevTerm> terms;
   std::vector<double> consts;
   std::vector<int> col_obs;
+  std::vector<int> term_pdf;
 
   int slot(int obs) {
     for (std::size_t i = 0; i < col_obs.size(); ++i) {
@@ -93,6 +94,7 @@ struct Emitter {
         usage_error("internal: not a leaf");
     }
     terms.push_back(t);
+    term_pdf.push_back(id);
   }
 
   // scale * unnorm(pdf) for a one-dimensional pdf, as a flat sum of leaves.
@@ -165,7 +167,7 @@ struct Emitter {
 }  // namespace
 
 HostPlan compile_plan(const Model& m, int pdf, bool normalized) {
-  Emitter e{m, nullptr, {}, {}, {}};
+  Emitter e{m, nullptr, {}, {}, {}, {}};
   e.root(pdf, 1.0);
   if (e.terms.size() > static_cast<std::size_t>(kMaxTerms)) {
     usage_error("model has " + std::to_string(e.terms.size()) + " leaf terms; the GPU plan holds " +
@@ -178,6 +180,7 @@ HostPlan compile_plan(const Model& m, int pdf, bool normalized) {
   hp.pdf = pdf;
   hp.normalized = normalized;
   hp.col_obs = e.col_obs;
+  hp.term_pdf = e.term_pdf;
   hp.dev.nterms = static_cast<int>(e.terms.size());
   hp.dev.ncols = static_cast<int>(e.col_obs.size());
   hp.dev.stride = static_cast<int>(e.consts.size());
@@ -211,10 +214,134 @@ void build_constants(const HostPlan& plan, const Model& m, const double* theta, 
   m.check_params(plan.pdf, theta);
   const double scale =
       (plan.normalized ? 1.0 / m.normalization(plan.pdf, theta) : 1.0) * extra_scale;
-  Emitter e{m, theta, {}, {}, {}};
+  Emitter e{m, theta, {}, {}, {}, {}};
   e.root(plan.pdf, scale);
   if (static_cast<int>(e.consts.size()) != plan.dev.stride) usage_error("internal: plan drift");
   for (int i = 0; i < plan.dev.stride; ++i) row[i] = e.consts[i];
+}
+
+namespace {
+
+// (value, d/d theta_j) pairs: the coefficient traversal differentiated forward
+struct Dual {
+  double v, d;
+};
+Dual operator*(Dual a, Dual b) { return {a.v * b.v, a.d * b.v + a.v * b.d}; }
+Dual operator/(Dual a, Dual b) { return {a.v / b.v, (a.d * b.v - a.v * b.d) / (b.v * b.v)}; }
+
+// Mirrors Emitter's traversal (same terms in the same order) carrying Duals.
+struct CoefGradEmitter {
+  const Model& m;
+  const double* theta;
+  int j;
+  std::vector<double> dcoef;
+
+  Dual norm(int pdf) const { return {m.normalization(pdf, theta), m.normalization_grad(pdf, theta, j)}; }
+  std::vector<Dual> fracs(int pdf) const {
+    const std::vector<double> f = m.fractions(pdf, theta), df = m.fractions_grad(pdf, theta, j);
+    std::vector<Dual> r(f.size());
+    for (std::size_t i = 0; i < f.size(); ++i) r[i] = {f[i], df[i]};
+    return r;
+  }
+  void sum(int id, Dual scale) {
+    const Pdf& p = m.pdfs[id];
+    if (is_leaf(p.kind)) {
+      dcoef.push_back(scale.d);
+    } else if (p.kind == Kind::ProdPdf && p.children.size() == 1) {
+      sum(p.children[0], scale);
+    } else {
+      const std::vector<Dual> f = fracs(id);
+      for (std::size_t i = 0; i < p.children.size(); ++i) sum(p.children[i], scale * (f[i] / norm(p.children[i])));
+    }
+  }
+  void factors(int id, std::vector<int>& out) const {
+    const Pdf& p = m.pdfs[id];
+    if (p.kind == Kind::ProdPdf) {
+      for (const int c : p.children) factors(c, out);
+    } else {
+      out.push_back(id);
+    }
+  }
+  void product(int id, Dual scale) {
+    std::vector<int> fs;
+    factors(id, fs);
+    for (std::size_t k = 0; k < fs.size(); ++k) sum(fs[k], k == 0 ? scale : Dual{1.0, 0.0});
+  }
+  void root(int id, Dual scale) {
+    const Pdf& p = m.pdfs[id];
+    if (p.kind == Kind::ProdPdf) {
+      product(id, scale);
+    } else if (p.obs >= 0) {
+      sum(id, scale);
+    } else {
+      const std::vector<Dual> f = fracs(id);
+      for (std::size_t i = 0; i < p.children.size(); ++i) {
+        const int c = p.children[i];
+        const Dual coef = scale * (f[i] / norm(c));
+        if (m.pdfs[c].kind == Kind::ProdPdf) {
+          product(c, coef);
+        } else {
+          sum(c, coef);
+        }
+      }
+    }
+  }
+};
+
+}  // namespace
+
+std::vector<double> coef_derivatives(const HostPlan& plan, const Model& m, const double* theta, int j,
+                                     double extra_scale) {
+  CoefGradEmitter e{m, theta, j, {}};
+  const Dual n = plan.normalized ? Dual{m.normalization(plan.pdf, theta), m.normalization_grad(plan.pdf, theta, j)}
+                                 : Dual{1.0, 0.0};
+  e.root(plan.pdf, Dual{extra_scale, 0.0} / n);
+  if (static_cast<int>(e.dcoef.size()) != plan.dev.nterms) usage_error("internal: gradient plan drift");
+  return e.dcoef;
+}
+
+GradPlan compile_grad_plan(const HostPlan& plan, const Model& m) {
+  GradPlan gp;
+  const DevPlan& d = plan.dev;
+  int slot = 1;
+  gp.slot_param.assign(1, -1);
+  int factor = 0, fbeg = 0;
+  for (int i = 0; i < d.nterms; ++i) {
+    DevGradTerm& g = gp.dev.g[i];
+    g.slot = slot++;
+    gp.slot_param.push_back(-1);
+    gp.a_slot.push_back(g.slot);
+    const Pdf& leaf = m.pdfs[plan.term_pdf[i]];
+    for (std::size_t k = 0; k < leaf.params.size(); ++k) {
+      if (m.params[leaf.params[k]].constant) continue;
+      g.pmask |= 1 << k;
+      gp.slot_param.push_back(leaf.params[k]);
+      ++slot;
+    }
+    g.factor = factor;
+    g.fbeg = fbeg;
+    if (d.t[i].flags & TF_END_SUM) ++factor;
+    if (d.t[i].flags & TF_END_PROD) {
+      // close the product: every term since fbeg's first term gets fend
+      for (int j = i; j >= 0 && gp.dev.g[j].fbeg == fbeg && gp.dev.g[j].fend == 0; --j) {
+        gp.dev.g[j].fend = factor;
+      }
+      fbeg = factor;
+    }
+  }
+  gp.dev.nslots = slot;
+  gp.dev.nfactors = factor;
+  if (slot > kMaxGradSlots) {
+    gp.why = "gradient layout needs " + std::to_string(slot) + " accumulators; the device pass holds " +
+             std::to_string(kMaxGradSlots);
+  } else if (factor > kMaxFactors) {
+    gp.why = "more than " + std::to_string(kMaxFactors) + " factors";
+  } else if (!plan.normalized) {
+    gp.why = "not a likelihood plan";
+  } else {
+    gp.ok = true;
+  }
+  return gp;
 }
 
 }  // namespace ffb

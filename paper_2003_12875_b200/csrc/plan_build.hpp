@@ -3,6 +3,7 @@
 // launch).  See plan.hpp for the canonical form.
 #pragma once
 
+#include <string>
 #include <vector>
 
 #include "model.hpp"
@@ -15,7 +16,28 @@ struct HostPlan {
   int pdf = -1;            // the pdf this plan evaluates
   bool normalized = true;  // true: p = unnorm / N (the likelihood); false: eval_batch
   std::vector<int> col_obs;  // compact column slot -> observable index
+  std::vector<int> term_pdf; // leaf pdf of each term
 };
+
+// Slot layout of the fused NLL + gradient pass (plan.hpp DevGradPlan) for the
+// model's free parameters.  `ok` false (with the reason) when the layout exceeds the
+// device limits; then only finite-difference gradients are available.
+struct GradPlan {
+  bool ok = false;
+  std::string why;
+  DevGradPlan dev{};
+  std::vector<int> slot_param;  // B slot -> parameter index (-1 for slot 0 / A slots)
+  std::vector<int> a_slot;      // term -> its A slot
+};
+
+GradPlan compile_grad_plan(const HostPlan& plan, const Model& m);
+
+// d coef_c / d theta_j for every term of the plan (the coefficients exactly as
+// build_constants writes them, extra_scale included): the constant builder's
+// traversal differentiated forward, with the normalisation derivatives of
+// model_grad.cpp.
+std::vector<double> coef_derivatives(const HostPlan& plan, const Model& m, const double* theta, int j,
+                                     double extra_scale);
 
 // Flattens `pdf` (the model root for the likelihood).  Throws Usage for trees
 // outside the canonical form (e.g. a ProdPdf nested in a 1-D sum).

@@ -135,6 +135,15 @@ class Model:
         _check(lib().ffcu_point_constants(self._h, None if p is None else _dp(p), _dp(row)))
         return row
 
+    def coef_derivatives(self, param, point=None):
+        """d coef_c / d theta[param] for every plan term (host logic of the gradient pass)."""
+        terms, _, _ = self.plan()
+        out = np.empty(len(terms))
+        p = None if point is None else _f64(point)
+        j = self.param_names.index(param) if isinstance(param, str) else int(param)
+        _check(lib().ffcu_coef_derivatives(self._h, None if p is None else _dp(p), j, _dp(out)))
+        return out
+
     def extended_terms(self, points, n_events):
         pts = _f64(np.atleast_2d(points))
         out = np.empty(pts.shape[0])
@@ -271,6 +280,52 @@ def nll_points(model: Model, ds: DataSet, points):
     return vals, bad, ne.value
 
 
+def nll_grad(model: Model, ds: DataSet, points=None):
+    """NLL and dNLL/dtheta (all parameters, 0 for constant ones) at P points in one
+    fused pass over the events.  points=None: the current values.  Returns
+    (values[P], grads[P, npar], first_invalid[P], kernel launches)."""
+    if points is None:
+        points = model.theta()
+    pts = _f64(np.atleast_2d(points))
+    P = pts.shape[0]
+    vals = np.empty(P)
+    grads = np.empty((P, pts.shape[1]))
+    bad = np.empty(P, dtype=np.int64)
+    ne = ctypes.c_ulonglong()
+    _check(lib().ffcu_nll_grad(model.handle, ds.handle, _dp(pts), P, _dp(vals), _dp(grads),
+                               bad.ctypes.data_as(ctypes.POINTER(LL)), ctypes.byref(ne)))
+    return vals, grads, bad, ne.value
+
+
+def grad_slot_count(model: Model) -> int:
+    n = ctypes.c_int()
+    _check(lib().ffcu_grad_slot_count(model.handle, ctypes.byref(n)))
+    return n.value
+
+
+def nll_grad_partial(model: Model, ds: DataSet, points):
+    """Uncombined per-slot Neumaier pairs (P x nslots x 2) of the gradient pass."""
+    pts = _f64(np.atleast_2d(points))
+    P = pts.shape[0]
+    sc = np.empty((P, grad_slot_count(model), 2))
+    bad = np.empty(P, dtype=np.int64)
+    _check(lib().ffcu_nll_grad_partial(model.handle, ds.handle, _dp(pts), P, _dp(sc),
+                                       bad.ctypes.data_as(ctypes.POINTER(LL)), None))
+    return sc, bad
+
+
+def nll_grad_finish(model: Model, points, slot_sums, n_events: float):
+    """Host finish of the gradient from combined slot sums (P x nslots)."""
+    pts = _f64(np.atleast_2d(points))
+    sums = _f64(np.atleast_2d(slot_sums))
+    P = pts.shape[0]
+    vals = np.empty(P)
+    grads = np.empty((P, pts.shape[1]))
+    _check(lib().ffcu_nll_grad_finish(model.handle, _dp(pts), P, _dp(sums), float(n_events),
+                                      _dp(vals), _dp(grads)))
+    return vals, grads
+
+
 def nll_points_partial(model: Model, ds: DataSet, points):
     """Uncombined Neumaier pairs (P x 2) of the event sum, for cross-rank combining."""
     pts = _f64(np.atleast_2d(points))
@@ -341,6 +396,7 @@ class FitResult:
     iterations: int = 0
     n_launches: int = 0
     trace: list = field(default_factory=list)
+    analytic_gradient: bool = False
 
     def value(self, name):
         return next(p.value for p in self.parameters if p.name == name)
@@ -358,7 +414,8 @@ def _result(h) -> FitResult:
         return FitResult(bool(L.ffit_result_converged(h)), L.ffit_result_nll(h), params,
                          int(L.ffit_result_nll_calls(h)), L.ffit_result_wall_seconds(h),
                          bool(L.ffit_result_uncertainties_valid(h)), L.ffcu_result_iterations(h),
-                         int(L.ffcu_result_launches(h)), list(tr[:n]))
+                         int(L.ffcu_result_launches(h)), list(tr[:n]),
+                         bool(L.ffcu_result_analytic_gradient(h)))
     finally:
         L.ffit_result_free(h)
 
@@ -370,10 +427,13 @@ def fit_to(model: Model, ds: DataSet, mode: EvalMode = EvalMode.Gpu, tolerance=0
     return _result(h)
 
 
-def fit_gradient(model: Model, ds: DataSet, tolerance=0.0, max_iterations=0) -> FitResult:
-    """Minuit-style BFGS on central differences: 2d+1 points per launch."""
+def fit_gradient(model: Model, ds: DataSet, tolerance=0.0, max_iterations=0, analytic=True) -> FitResult:
+    """Minuit-style BFGS.  analytic=True: gradients from the fused NLL + gradient pass
+    (one point per iteration) when the model's layout fits it; False: central
+    differences, 2d+1 points per launch."""
     h = VP()
-    _check(lib().ffcu_fit_gradient(model.handle, ds.handle, tolerance, max_iterations, ctypes.byref(h)))
+    _check(lib().ffcu_fit_gradient_opts(model.handle, ds.handle, tolerance, max_iterations,
+                                        1 if analytic else 0, ctypes.byref(h)))
     return _result(h)
 
 

@@ -52,20 +52,27 @@ def test_nelder_mead_matches_reference_fit(name):
     assert r.n_launches < r.n_nll_calls  # independent points were batched
 
 
+@pytest.mark.parametrize("analytic", [False, True], ids=["fd", "analytic"])
 @pytest.mark.parametrize("name", list(FIT_CASES))
-def test_gradient_fit_reaches_reference_minimum(name):
+def test_gradient_fit_reaches_reference_minimum(name, analytic):
     case, gold = FIT_CASES[name], GOLD[name]
     ds, _ = data_for(case)
     m = start_model(case)
-    r = fb.fit_gradient(m, ds, tolerance=1e-12, max_iterations=200)
+    r = fb.fit_gradient(m, ds, tolerance=1e-12, max_iterations=200, analytic=analytic)
     assert r.converged
+    assert r.analytic_gradient == analytic
     for p in r.parameters:
         want, unc = gold["params"][p.name]
         assert abs(p.value - want) <= max(1e-6, 2e-3 * unc), (p.name, p.value, want)
     assert r.nll_min <= gold["nll"] + 1e-7
     d = len(r.parameters)
-    # every iteration is one launch of 2d+1 points (plus the one Hessian launch)
-    assert r.n_nll_calls == (r.n_launches - 1) * (2 * d + 1) + (1 + 2 * d + 2 * d * (d - 1))
+    hess = 1 + 2 * d + 2 * d * (d - 1)  # the one Hessian launch
+    if analytic:
+        # the start launch (centre + 2d gradient points), then one point per launch
+        assert r.n_nll_calls == (2 * d + 1) + (r.n_launches - 2) + hess
+    else:
+        # every iteration is one launch of 2d+1 points
+        assert r.n_nll_calls == (r.n_launches - 1) * (2 * d + 1) + hess
 
 
 def test_fit_nll_matches_oracle_at_minimum():

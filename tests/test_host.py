@@ -221,3 +221,55 @@ def test_gpu_calls_fail_loudly_without_device():
     with pytest.raises(fb.FfitError) as e:
         fb.DataSet.from_columns({"x": np.zeros(10)})
     assert e.value.code == 3 and "CUDA" in e.value.message
+
+
+def test_gradient_slot_layout():
+    """Accumulators of the fused NLL + gradient pass (plan.hpp DevGradPlan): slot 0, then
+    per term one A slot plus one B slot per FREE leaf parameter."""
+    from paper_2003_12875_b200 import configs
+    # C2: Gaussian (m, s free) + ArgusBG (m0, p const; c free)
+    assert fb.grad_slot_count(fb.Model.from_string(configs.C2.text)) == 1 + 3 + 2
+    # C5: m0 free too
+    assert fb.grad_slot_count(fb.Model.from_string(configs.C5.text)) == 1 + 3 + 3
+    # C4: 5 Gaussians (2 each) + Exponential (1)
+    assert fb.grad_slot_count(fb.Model.from_string(configs.C4.text)) == 1 + 5 * 3 + 2
+    # C3: Gaussian, Exponential, Chebychev-3
+    assert fb.grad_slot_count(fb.Model.from_string(configs.C3.text)) == 1 + 3 + 2 + 4
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5", "johnson", "mix_chisq"])
+def test_coefficient_derivatives(name):
+    """d coef_c / d theta_j of the gradient pass's host side against 4-point differences
+    of the constant builder at several steps (the closest one: the builder's own
+    rounding bounds the difference quotients, not the analytic side)."""
+    from paper_2003_12875_b200 import configs
+    from tests.models import REF_MODELS
+    text = {"c2": configs.C2.text, "c3": configs.C3.text, "c4": configs.C4.text, "c5": configs.C5.text,
+            "johnson": REF_MODELS["johnson"][0], "mix_chisq": REF_MODELS["mix_chisq"][0]}[name]
+    m = fb.Model.from_string(text)
+    terms, _, _ = m.plan()
+    coffs = [t["coff"] for t in terms]
+    th = m.theta()
+    spans = {}
+    for line in text.splitlines():
+        t = line.split()
+        if t and t[0] == "parameter":
+            spans[t[1]] = (float(t[4]) - float(t[3]), len(t) > 5)
+    base = np.abs(m.point_constants(th)[coffs])
+    for j, pn in enumerate(m.param_names):
+        span, const = spans[pn]
+        if const:
+            continue
+        d = m.coef_derivatives(j, th)
+        ests = []
+        for hr in (1e-6, 3e-6, 1e-5, 3e-5, 1e-4):
+            h = hr * span
+
+            def C(dx):
+                t = th.copy()
+                t[j] += dx
+                return m.point_constants(t)[coffs]
+
+            ests.append((8 * (C(h) - C(-h)) - (C(2 * h) - C(-2 * h))) / (12 * h))
+        err = np.min(np.abs(np.array(ests) - d), axis=0)
+        assert np.all(err <= 1e-9 * np.maximum(np.abs(d), base)), (pn, err)
