@@ -396,7 +396,8 @@ def run_fit(args, w):
     fb.kernel_timer(True)
     fb.kernel_timer_read()
     launches0 = fb.kernel_launches()
-    r = fb.fit_gradient(model, ds, tolerance=1e-12, max_iterations=args.iterations)
+    analytic = args.gradient == "analytic"
+    r = fb.fit_gradient(model, ds, tolerance=1e-12, max_iterations=args.iterations, analytic=analytic)
     torch.cuda.synchronize()
     kms, kcount = fb.kernel_timer_read()
     launches = fb.kernel_launches() - launches0
@@ -407,11 +408,14 @@ def run_fit(args, w):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded generator, reference Rng)",
         "config": {"workload": w.name, "description": w.description, "events_per_gpu": n,
-                   "points_per_launch": 2 * d + 1, "free_parameters": d},
+                   "gradient": "analytic (fused NLL + gradient pass, one point per launch)" if r.analytic_gradient
+                   else "central differences (2d+1 points per launch)",
+                   "points_per_launch": 1 if r.analytic_gradient else 2 * d + 1, "free_parameters": d},
         "fit": {"converged": r.converged, "iterations": r.iterations, "launches": r.n_launches,
                 "nll_evaluations": r.n_nll_calls, "nll_evaluations_per_s": r.n_nll_calls / r.wall_seconds,
                 "wall_seconds": r.wall_seconds, "kernel_ms_total": kms, "kernel_launches_timed": kcount,
-                "nll_min": r.nll_min,
+                "nll_min": r.nll_min, "analytic_gradient": r.analytic_gradient,
+                "kernel_ms_per_launch": kms / max(kcount, 1),
                 "parameters": {p.name: [p.value, p.uncertainty] for p in r.parameters},
                 "truth": dict(zip(truth.param_names, [float(v) for v in truth.theta()])),
                 "data_generation_s": t_gen},
@@ -455,6 +459,9 @@ def main():
     ap.add_argument("--force-collective", action="store_true",
                     help="run the NCCL all-gather + combine exchange even at N = 1")
     ap.add_argument("--iterations", type=int, default=50, help="fit iterations (--fit / c5)")
+    ap.add_argument("--gradient", default="fd", choices=["fd", "analytic"],
+                    help="c5 fit gradients: central differences (the config's 2d+1 points per launch) "
+                         "or the fused NLL + gradient pass")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

@@ -200,6 +200,8 @@ int ffcu_fit_gradient_opts(ffit_model* m, const ffit_dataset* ds, double toleran
 /* 1 if the fit's gradients came from the fused pass. */
 int ffcu_result_analytic_gradient(const ffit_fit_result* r);
 int ffcu_result_iterations(const ffit_fit_result* r);
+/* fit_gradient: the last estimated distance to the minimum, g^T H^-1 g / 2. */
+double ffcu_result_edm(const ffit_fit_result* r);
 unsigned long long ffcu_result_launches(const ffit_fit_result* r);
 int ffcu_result_trace(const ffit_fit_result* r, double* out, int cap);
 

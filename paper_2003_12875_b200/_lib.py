@@ -92,6 +92,7 @@ SIGNATURES = {
     "ffcu_fit_gradient_opts": (I, [VP, VP, D, ctypes.c_long, I, ctypes.POINTER(VP)]),
     "ffcu_result_analytic_gradient": (I, [VP]),
     "ffcu_result_iterations": (I, [VP]),
+    "ffcu_result_edm": (D, [VP]),
     "ffcu_result_launches": (ULL, [VP]),
     "ffcu_result_trace": (I, [VP, DP, I]),
     "ffcu_last_launch": (I, [VP, IP]),

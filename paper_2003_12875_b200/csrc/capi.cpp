@@ -753,6 +753,7 @@ FFB_API double ffit_result_param_uncertainty(const ffit_fit_result* r, int i) {
 FFB_API void ffit_result_free(ffit_fit_result* r) { delete r; }
 
 FFB_API int ffcu_result_iterations(const ffit_fit_result* r) { return r->r.iterations; }
+FFB_API double ffcu_result_edm(const ffit_fit_result* r) { return r->r.edm; }
 FFB_API unsigned long long ffcu_result_launches(const ffit_fit_result* r) { return r->r.n_launches; }
 FFB_API int ffcu_result_trace(const ffit_fit_result* r, double* out, int cap) {
   const int n = static_cast<int>(r->r.trace.size());

@@ -417,8 +417,17 @@ NllGradResult Engine::nll_grad_points(const DeviceDataset& ds, const double* the
       ColPtrs cols;
       bind_columns(plan_, ds, cols);
       const int ks = plan_kind_set(plan_.dev, h_consts_[slot_], np);
-      const NllLaunchInfo li =
-          launch_nll_grad(plan_.dev, gp.dev, cols, ds.n, d_consts, np, d_scratch_, d_gslots_, d_bad_, stream_, ks);
+      cudaEvent_t ea = nullptr, eb = nullptr;
+      {
+        std::lock_guard<std::mutex> lk(g_timer_mu);
+        if (g_timer_on) {
+          cuda_check(cudaEventCreate(&ea), "cudaEventCreate");
+          cuda_check(cudaEventCreate(&eb), "cudaEventCreate");
+          g_timer_events.emplace_back(ea, eb);
+        }
+      }
+      const NllLaunchInfo li = launch_nll_grad(plan_.dev, gp.dev, cols, ds.n, d_consts, np, d_scratch_, d_gslots_,
+                                               d_bad_, stream_, ks, ea, eb);
       cuda_check(cudaGetLastError(), "launch_nll_grad");
       r.launches += li.launches;
       count_launches(li.launches);

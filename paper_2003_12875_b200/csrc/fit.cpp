@@ -3,6 +3,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <limits>
 #include <numeric>
 
@@ -345,6 +347,9 @@ struct GradObjective {
 
 }  // namespace
 
+// Rounding resolution of an NLL value: a few ulps of |f|.
+static double resolution(double f) { return 4.0 * std::numeric_limits<double>::epsilon() * std::fabs(f); }
+
 FitResult fit_gradient(Model& m, Engine& e, const DeviceDataset& ds, const FitOptions& o) {
   const auto t0 = std::chrono::steady_clock::now();
   BatchObjective f{m, e, ds, m.free_parameters()};
@@ -361,6 +366,7 @@ FitResult fit_gradient(Model& m, Engine& e, const DeviceDataset& ds, const FitOp
   int backtracks = 0, iter = 0;
   FitResult result;
   result.analytic_gradient = analytic;
+  const bool debug = std::getenv("FFB_FIT_DEBUG") != nullptr;
   std::vector<double> fv;
   std::vector<std::vector<double>> gv;
   for (; iter < o.max_iterations; ++iter) {
@@ -393,6 +399,13 @@ FitResult fit_gradient(Model& m, Engine& e, const DeviceDataset& ds, const FitOp
       f0 = fv[0];
       g = gv[0];
       if (!std::isfinite(f0) || f0 > f_prev) {
+        if (debug) std::fprintf(stderr, "[fit_gradient] iter %d f %.17g > %.17g: backtrack\n", iter, f0, f_prev);
+        // a rise inside the NLL's own rounding after the model already predicted a
+        // gain below it: the minimum is resolved as far as the NLL can resolve it
+        if (f0 - f_prev <= resolution(f_prev) && result.edm <= 100.0 * resolution(f_prev)) {
+          converged = true;
+          break;
+        }
         if (++backtracks > 40) break;
         for (std::size_t i = 0; i < d; ++i) u[i] = u_prev[i] + 0.5 * (u[i] - u_prev[i]);
         continue;
@@ -432,7 +445,12 @@ FitResult fit_gradient(Model& m, Engine& e, const DeviceDataset& ds, const FitOp
       for (std::size_t j = 0; j < d; ++j) step[i] -= H[i][j] * g[j];
       edm -= 0.5 * g[i] * step[i];
     }
-    if (edm < o.tolerance && have_prev) {
+    result.edm = edm;
+    if (debug) std::fprintf(stderr, "[fit_gradient] iter %d f %.17g edm %.3g\n", iter, f0, edm);
+    // EDM below the tolerance, or below what the NLL value itself resolves (a
+    // 2e8-event NLL ~ 5e8 carries ~1e-7 of rounding: a tolerance of 1e-12 is then
+    // unreachable, as Minuit's "EDM below machine accuracy")
+    if ((edm < o.tolerance || edm < resolution(f0)) && have_prev) {
       converged = true;
       break;
     }

@@ -42,6 +42,7 @@ struct FitResult {
   double wall_seconds = 0.0;
   bool uncertainties_valid = true;
   bool analytic_gradient = false;  // fit_gradient used the fused gradient pass
+  double edm = 0.0;                // fit_gradient: last estimated distance to minimum
   std::vector<double> trace;
 };
 

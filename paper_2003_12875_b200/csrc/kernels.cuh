@@ -52,7 +52,8 @@ NllLaunchInfo launch_nll(const DevPlan& plan, const ColPtrs& cols, long long n,
 // point p and slot q, out[p * gp.nslots + q] = (s, c); bad as launch_nll.
 NllLaunchInfo launch_nll_grad(const DevPlan& plan, const DevGradPlan& gp, const ColPtrs& cols,
                               long long n, const double* d_consts, int P, void* scratch,
-                              SumPair* d_out, unsigned long long* d_bad, cudaStream_t stream, int ks);
+                              SumPair* d_out, unsigned long long* d_bad, cudaStream_t stream, int ks,
+                              cudaEvent_t ev_start = nullptr, cudaEvent_t ev_stop = nullptr);
 std::size_t nll_grad_scratch_bytes(long long n, int P, const DevPlan& plan, const DevGradPlan& gp);
 // Whether the gradient pass's shared-memory layout fits a CTA.
 bool grad_layout_fits(const DevPlan& plan, const DevGradPlan& gp);

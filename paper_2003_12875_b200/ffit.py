@@ -397,6 +397,7 @@ class FitResult:
     n_launches: int = 0
     trace: list = field(default_factory=list)
     analytic_gradient: bool = False
+    edm: float = 0.0
 
     def value(self, name):
         return next(p.value for p in self.parameters if p.name == name)
@@ -415,7 +416,7 @@ def _result(h) -> FitResult:
                          int(L.ffit_result_nll_calls(h)), L.ffit_result_wall_seconds(h),
                          bool(L.ffit_result_uncertainties_valid(h)), L.ffcu_result_iterations(h),
                          int(L.ffcu_result_launches(h)), list(tr[:n]),
-                         bool(L.ffcu_result_analytic_gradient(h)))
+                         bool(L.ffcu_result_analytic_gradient(h)), float(L.ffcu_result_edm(h)))
     finally:
         L.ffit_result_free(h)
 
