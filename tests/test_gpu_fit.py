@@ -65,11 +65,15 @@ def test_gradient_fit_reaches_reference_minimum(name, analytic):
         want, unc = gold["params"][p.name]
         assert abs(p.value - want) <= max(1e-6, 2e-3 * unc), (p.name, p.value, want)
     assert r.nll_min <= gold["nll"] + 1e-7
+    assert r.uncertainties_valid
+    for p in r.parameters:  # the reference's Hessian uncertainties
+        assert p.uncertainty == pytest.approx(gold["params"][p.name][1], rel=1e-3)
     d = len(r.parameters)
     hess = 1 + 2 * d + 2 * d * (d - 1)  # the one Hessian launch
     if analytic:
-        # the start launch (centre + 2d gradient points), then one point per launch
-        assert r.n_nll_calls == (2 * d + 1) + (r.n_launches - 2) + hess
+        # the start launch (centre + 2d gradient points), one point per launch, then the
+        # Hessian from the gradients at u +- h e_i (2d points, one launch)
+        assert r.n_nll_calls == (2 * d + 1) + (r.n_launches - 2) + 2 * d
     else:
         # every iteration is one launch of 2d+1 points
         assert r.n_nll_calls == (r.n_launches - 1) * (2 * d + 1) + hess

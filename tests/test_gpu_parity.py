@@ -442,3 +442,32 @@ def test_c3_full_size_three_columns():
     assert np.all(np.abs(comb - vals) <= NLL_TOL * np.abs(vals))
     _, comp, _ = o.nll(cols, pts[0])
     assert abs(vals[0] - comp) <= NLL_TOL * abs(comp)
+
+
+def test_streaming_and_tile_kernels_agree():
+    """Launches of <= 8 points over aligned columns take the persistent streaming kernel,
+    larger ones the tile-per-CTA kernel: same values to summation-order rounding."""
+    w = configs.C2
+    m, ds, cols, o = setup(w.text, 333_333, 21)
+    pts = w.points(m, n_points=9)
+    many, _, _ = fb.nll_points(m, ds, pts)           # tile kernel (P = 9)
+    assert fb.last_launch(m)["nchunks"] > 0
+    for p in range(9):
+        one, _, _ = fb.nll_points(m, ds, pts[p])      # streaming kernel (P = 1)
+        assert fb.last_launch(m)["nchunks"] == 0
+        assert abs(one[0] - many[p]) <= 1e-13 * abs(many[p])
+        _, comp, _ = o.nll(cols, pts[p])
+        assert abs(one[0] - comp) <= NLL_TOL * abs(comp)
+    few, _, _ = fb.nll_points(m, ds, pts[:8])         # streaming, several points
+    assert np.all(np.abs(few - many[:8]) <= 1e-13 * np.abs(many[:8]))
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 2047, 2048, 2049, 4097, 606_209])
+def test_streaming_ragged_sizes(n):
+    """Odd final elements (patched after the even-length bulk copy), fewer tiles than
+    CTAs, and a tile count that is not a multiple of the grid."""
+    m, ds, cols, o = setup(MIX, n, n)
+    v = fb.nll(m, ds)
+    _, comp, _ = o.nll(cols)
+    assert abs(v.value - comp) <= NLL_TOL * abs(comp)
+    assert v.first_invalid == -1
