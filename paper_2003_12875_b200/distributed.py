@@ -10,6 +10,11 @@ rank.  The extended term (nu - N log nu) is added once, with the global N.
 The same combine runs on the host (numpy) for the CPU/gloo tests and on the device
 (ffcu_combine_pairs_device) on the GPU path; both apply the identical sequence of
 fp64 operations.
+
+Gradients shard the same way: the fused NLL + gradient pass yields per point a row of
+slot sums (plan.hpp DevGradPlan: the NLL, one A_c per term, one B per free leaf
+parameter), all event sums; the ranks exchange their slot pairs, combine them in rank
+order and finish on the host with the global event count (ffcu_nll_grad_finish).
 """
 from __future__ import annotations
 
@@ -45,6 +50,20 @@ def combine_pairs(pairs_by_rank: np.ndarray) -> np.ndarray:
             c += float(pairs_by_rank[r, p, 1])
         out[p] = (s, c)
     return out
+
+
+def combine_slots(slots_by_rank: np.ndarray) -> np.ndarray:
+    """[R, P, S, 2] gradient slot pairs -> [P, S] combined sums (rank order)."""
+    R, P, S, _ = slots_by_rank.shape
+    c = combine_pairs(slots_by_rank.reshape(R, P * S, 2))
+    return (c[:, 0] + c[:, 1]).reshape(P, S)
+
+
+def finalize_grad(values: np.ndarray, grads: np.ndarray, bad: np.ndarray):
+    """+inf values and NaN gradients where an event was invalid."""
+    v = np.where(bad >= 0, np.inf, values)
+    g = np.where((bad >= 0)[:, None], np.nan, grads)
+    return v, g
 
 
 def first_invalid_global(bad_by_rank: np.ndarray, offsets) -> np.ndarray:
@@ -105,3 +124,29 @@ class ShardedNll:
         bad = first_invalid_global(bads.view(self.world, P).cpu().numpy(), offs.cpu().numpy())
         ext = self.model.extended_terms(pts, self.n_total)
         return finalize(combined.cpu().numpy(), bad, ext)
+
+    def nll_grad(self, points: np.ndarray):
+        """(values[P], grads[P, npar]) over all ranks' shards: per-rank slot pairs,
+        one all-gather, rank-order combine, host finish with the global N."""
+        from . import ffit as fb
+
+        torch = self.torch
+        pts = np.atleast_2d(points)
+        sc, bad = fb.nll_grad_partial(self.model, self.ds, pts)
+        P, S, _ = sc.shape
+        if self.world > 1:
+            t = torch.from_numpy(np.ascontiguousarray(sc)).to(self.device)
+            gathered = torch.empty((self.world,) + tuple(t.shape), dtype=torch.float64, device=self.device)
+            self.dist.all_gather_into_tensor(gathered, t)
+            tb = torch.from_numpy(bad).to(self.device)
+            bads = torch.empty((self.world, P), dtype=torch.int64, device=self.device)
+            self.dist.all_gather_into_tensor(bads, tb)
+            offs = torch.empty(self.world, dtype=torch.int64, device=self.device)
+            self.dist.all_gather_into_tensor(offs, torch.tensor([self.offset], device=self.device))
+            sums = combine_slots(gathered.cpu().numpy())
+            gbad = first_invalid_global(bads.cpu().numpy(), offs.cpu().numpy())
+        else:
+            sums = combine_slots(sc[None])
+            gbad = bad
+        vals, grads = fb.nll_grad_finish(self.model, pts, sums, self.n_total)
+        return finalize_grad(vals, grads, gbad)

@@ -104,3 +104,105 @@ def test_first_invalid_global_index():
     assert list(D.first_invalid_global(bad, [0, 100])) == [103, 5]
     vals = D.finalize(np.zeros((2, 2)), np.array([-1, 7]), np.zeros(2))
     assert vals[0] == 0 and np.isinf(vals[1])
+
+
+def _c2_slots(o, names, coefs, cols_x, theta):
+    """Numpy restatement of the gradient pass's slot sums for the C2 model (Gaussian m, s
+    free; ArgusBG c free): slot 0 = sum -log p, A_c = sum leaf_c / p', B = sum coef dleaf / p,
+    p' = p * 2^54 as on the device (the host finish applies 2^54-scaled coefficient
+    derivatives)."""
+    import math
+    x = cols_x
+    th = dict(zip(names, theta))
+    g = np.exp(-(x - th["m"]) ** 2 / (2 * th["s"] ** 2))
+    t = 1 - (x / th["m0"]) ** 2
+    a = np.where(t > 0, x * np.sqrt(np.maximum(t, 0)) * np.exp(th["c"] * t), 0.0)
+    p = coefs[0] * g + coefs[1] * a
+    d = x - th["m"]
+    rows = [
+        -np.log(p),
+        g / p / 2.0 ** 54,
+        coefs[0] * g * d / th["s"] ** 2 / p,
+        coefs[0] * g * d * d / th["s"] ** 3 / p,
+        a / p / 2.0 ** 54,
+        coefs[1] * a * np.where(t > 0, t, 0.0) / p,
+    ]
+    return np.array([[math.fsum(r), 0.0] for r in rows])
+
+
+def _grad_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import torch
+
+    import paper_2003_12875_b200 as fb
+    from oracle.oracle import OracleModel
+    from paper_2003_12875_b200 import configs
+
+    w = configs.C2
+    m = fb.Model.from_string(w.text)
+    o = OracleModel(w.text)
+    n = 20_001
+    cols, _ = o.sample(n, 3)
+    th = w.points(m, n_points=2)[1]
+    terms, _, _ = m.plan()
+    coefs = m.point_constants(th)[[t["coff"] for t in terms]]
+    assert fb.grad_slot_count(m) == 6
+    b, e = D.shard_bounds(n, world, rank)
+    local = _c2_slots(o, m.param_names, coefs, cols[0][b:e], th)[None]  # [P=1, S, 2]
+    t = torch.from_numpy(local)
+    gathered = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(gathered, t)
+    sums = D.combine_slots(np.stack([g.numpy() for g in gathered]))
+    vals, grads = fb.nll_grad_finish(m, th[None], sums, n)
+    if rank == 0:
+        q.put((vals, grads, th, cols[0]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_gloo_sharded_gradient():
+    """Shard slot sums (numpy restatement), exchange over gloo, rank-order combine, the
+    product's host finish with the global N: equal to the oracle NLL and its gradient."""
+    import math
+
+    from oracle.oracle import OracleModel
+    from paper_2003_12875_b200 import configs
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_grad_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    vals, grads, th, x = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    o = OracleModel(configs.C2.text)
+    _, comp, _ = o.nll([x], th)
+    assert abs(vals[0] - comp) <= 1e-12 * abs(comp)
+    import paper_2003_12875_b200 as fb
+    names = fb.Model.from_string(configs.C2.text).param_names
+    p0 = o.probabilities([x], th)
+    for j, name in enumerate(names):
+        if name in ("m0", "p"):
+            assert grads[0, j] == 0.0
+            continue
+        h = 1e-4 * {"m": 0.09, "s": 0.009, "c": 99.0, "f": 1.0}[name]
+
+        def P(dx):
+            t = th.copy()
+            t[j] += dx
+            return o.probabilities([x], t)
+
+        dl = (8 * (P(h) - P(-h)) - (P(2 * h) - P(-2 * h))) / (12 * h) / p0
+        want = -math.fsum(dl)
+        assert abs(grads[0, j] - want) <= 1e-8 * np.sum(np.abs(dl)), (name, grads[0, j], want)
+
+
+def test_finalize_grad_marks_invalid_points():
+    v, g = D.finalize_grad(np.array([1.0, 2.0]), np.ones((2, 3)), np.array([-1, 4]))
+    assert v[0] == 1.0 and np.isinf(v[1])
+    assert np.all(g[0] == 1.0) and np.all(np.isnan(g[1]))

@@ -269,3 +269,19 @@ def test_partial_and_finish_equal_the_one_call():
     assert abs(v[0] - v_all[0]) <= NLL_TOL * abs(v_all[0])
     g_ref, scale, _ = ref_gradient(text, cols, th, m.param_names, 40_000, yields_of(text))
     assert np.all(np.abs(g[0] - g_all[0]) <= GRAD_TOL * scale)
+
+
+def test_sharded_gradient_single_rank_equals_direct():
+    """distributed.ShardedNll.nll_grad on one rank (no process group) reproduces nll_grad."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2003_12875_b200 import distributed as D
+    text = configs.C5.text
+    m, ds, cols = setup(text, 70_001)
+    th = jittered(m, text, seed=11)
+    v0, g0, _, _ = fb.nll_grad(m, ds, th)
+    sh = D.ShardedNll(m, ds, 70_001, 0, dist, torch.device("cuda:0"))
+    v, g = sh.nll_grad(th)
+    assert abs(v[0] - v0[0]) <= 1e-15 * abs(v0[0])
+    assert np.allclose(g[0], g0[0], rtol=1e-14, atol=0)
