@@ -1,8 +1,7 @@
+set -x
+python -m pytest tests -m gpu -q -x 2>&1 | tail -3
 for w in c2 c1 c4 c3; do
-for tag in base cbank base cbank; do
-  if [ $tag = base ]; then unset FFB_LIB_VARIANT; else export FFB_LIB_VARIANT=$tag; fi
-  python bench.py --workload $w --no-cpu-baseline --steps 20 > gpurun_out/ab_${w}_${tag}_$RANDOM.json 2>> gpurun_out/ab_err.log
+  python bench.py --workload $w --no-cpu-baseline --steps 20 > gpurun_out/b_${w}.json 2>> gpurun_out/b_err.log
+  python -c "import json;d=json.load(open('gpurun_out/b_${w}.json'));print('$w', '%.4e'%d['value'], d['roofline']['frac'], d['e2e']['value'])"
 done
-unset FFB_LIB_VARIANT
-done
-echo done
+python tools/small_p_bench.py
