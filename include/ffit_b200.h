@@ -184,6 +184,12 @@ int ffcu_point_constants(const ffit_model* m, const double* point, double* row);
 /* d coef_c / d theta_param for each plan term c (the row's coefficient entries;
  * host logic of the gradient pass, no GPU needed). */
 int ffcu_coef_derivatives(const ffit_model* m, const double* point, int param, double* out);
+/* The Expression formula language (proj/docs/expression-grammar.md):
+ * compile `text` over `nvars` variable names and evaluate it on the host at npts rows
+ * of values (row-major npts x nvars).  FFIT_ERR_USAGE with the reference's messages on
+ * syntax / unknown identifier / unknown function / arity errors. */
+int ffcu_expr_eval(const char* text, const char* const* vars, int nvars, const double* values, int npts,
+                   double* out);
 int ffcu_model_pdf_count(const ffit_model* m);
 const char* ffcu_model_pdf_name(const ffit_model* m, int i);
 int ffcu_model_observable_count(const ffit_model* m);

@@ -277,3 +277,14 @@ def ref_rng_gauss(seed, n):
     out = np.empty(n)
     ref().ref_rng_gauss(ctypes.c_ulonglong(seed), _LL(n), _dp(out))
     return out
+
+
+def ref_expr_eval(text, variables, values):
+    """The reference's compiled formula at rows of variable values (npts x nvars)."""
+    vals = np.ascontiguousarray(np.atleast_2d(values), dtype=np.float64)
+    arr = (ctypes.c_char_p * len(variables))(*[v.encode() for v in variables])
+    out = np.empty(vals.shape[0])
+    rc = ref().ref_expr_eval(text.encode(), arr, len(variables), _dp(vals), vals.shape[0], _dp(out))
+    if rc:
+        raise OracleError(rc, ref().ref_last_error().decode())
+    return out

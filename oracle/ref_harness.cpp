@@ -11,6 +11,7 @@
 //   normalization                   (proj/include/ffit/eval.hpp:26, src/eval.cpp:71-86)
 //   sample                          (proj/include/ffit/sampling.hpp, src/sampling.cpp:172-197)
 //   fit_to                          (proj/include/ffit/fit.hpp:47, src/fit.cpp:86-251)
+//   expr::compile / Program::eval   (proj/include/ffit/expr.hpp:128-135)
 // Exported symbols are prefixed `ref_`; every reference symbol stays hidden
 // (-fvisibility=hidden) so this library can share a process with the
 // product's `ffit_*` exports.
@@ -26,6 +27,7 @@
 #include <vector>
 
 #include "ffit/eval.hpp"
+#include "ffit/expr.hpp"
 #include "ffit/fit.hpp"
 #include "ffit/model.hpp"
 #include "ffit/sampling.hpp"
@@ -231,6 +233,20 @@ REF_API int ref_nll_points_threaded(const char* text, ref_dataset* d, int mode,
     for (auto& th : pool) th.join();
     for (const auto& e : errs) {
       if (!e.empty()) throw ffit::Error(ffit::ErrorCode::Numeric, e);
+    }
+  });
+}
+
+// One formula over `nvars` variables: compile, then evaluate the scalar program at `npts`
+// rows of values (row-major npts x nvars).  Errors carry the reference's messages.
+REF_API int ref_expr_eval(const char* text, const char* const* vars, int nvars, const double* values,
+                          int npts, double* out) {
+  return guarded([&] {
+    std::vector<std::string> names(vars, vars + nvars);
+    const ffit::expr::Program prog = ffit::expr::compile(std::string(text), names);
+    for (int i = 0; i < npts; ++i) {
+      out[i] = prog.eval(std::span<const double>(values + static_cast<std::size_t>(i) * nvars,
+                                                 static_cast<std::size_t>(nvars)));
     }
   });
 }

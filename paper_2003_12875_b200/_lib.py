@@ -84,6 +84,7 @@ SIGNATURES = {
     "ffcu_plan_term": (I, [VP, I, IP, IP, IP, IP, IP]),
     "ffcu_point_constants": (I, [VP, DP, DP]),
     "ffcu_coef_derivatives": (I, [VP, DP, I, DP]),
+    "ffcu_expr_eval": (I, [CP, ctypes.POINTER(CP), I, DP, I, DP]),
     "ffcu_model_pdf_count": (I, [VP]),
     "ffcu_model_pdf_name": (CP, [VP, I]),
     "ffcu_model_observable_count": (I, [VP]),

@@ -588,6 +588,23 @@ FFB_API int ffcu_coef_derivatives(const ffit_model* m, const double* point, int 
   });
 }
 
+FFB_API int ffcu_expr_eval(const char* text, const char* const* vars, int nvars, const double* values, int npts,
+                           double* out) {
+  return guarded([&] {
+    require(text, "text");
+    if (nvars < 0 || npts < 0) ffb::usage_error("nvars and npts must be >= 0");
+    if (nvars > 0) require(vars, "vars");
+    if (npts > 0) {
+      require(values, "values");
+      require(out, "out");
+    }
+    std::vector<std::string> names;
+    for (int i = 0; i < nvars; ++i) names.emplace_back(vars[i]);
+    const ffb::ExprProgram prog = ffb::compile_expression(text, names);
+    for (int i = 0; i < npts; ++i) out[i] = prog.eval(values + static_cast<std::size_t>(i) * nvars);
+  });
+}
+
 FFB_API int ffcu_model_pdf_count(const ffit_model* m) { return static_cast<int>(m->m->pdfs.size()); }
 
 FFB_API const char* ffcu_model_pdf_name(const ffit_model* m, int i) {

@@ -171,6 +171,7 @@ Engine::~Engine() {
     cudaFreeHost(h_bad_);
     cudaFree(d_gslots_);
     cudaFreeHost(h_gslots_);
+    cudaFree(d_prog_);
     if (stream_) cudaStreamDestroy(stream_);
     cudaSetDevice(prev);
   }
@@ -188,6 +189,12 @@ void Engine::ensure(int device, int P, std::size_t scratch) {
     cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
     for (int k = 0; k < 2; ++k) {
       cuda_check(cudaEventCreateWithFlags(&staged_[k], cudaEventDisableTiming), "cudaEventCreate");
+    }
+    if (!plan_.programs.empty()) {  // Expression programs: once per engine and device
+      const std::size_t bytes = plan_.programs.size() * sizeof(ExprInstr);
+      cuda_check(cudaMalloc(&d_prog_, bytes), "cudaMalloc(programs)");
+      cuda_check(cudaMemcpy(d_prog_, plan_.programs.data(), bytes, cudaMemcpyHostToDevice), "cudaMemcpy(programs)");
+      plan_.dev.prog = d_prog_;
     }
   }
   if (P > cap_points_) {
@@ -466,11 +473,19 @@ void Engine::probabilities(const DeviceDataset& ds, const double* theta, double*
 
 void Engine::eval_batch(int pdf, const DeviceDataset& ds, const double* theta, double* out,
                         bool out_on_device, cudaStream_t stream) {
-  const HostPlan plan = pdf < 0 ? plan_ : compile_plan(m_, pdf, false);
+  HostPlan plan = pdf < 0 ? plan_ : compile_plan(m_, pdf, false);
   m_.check_params(plan.pdf, theta);
   if (ds.n == 0) return;
   DeviceGuard g(ds.device);
   ensure(ds.device, 1, 0);
+  if (pdf < 0) plan.dev.prog = plan_.dev.prog;
+  ExprInstr* d_sub_prog = nullptr;  // a sub-pdf's own Expression programs (freed below)
+  if (pdf >= 0 && !plan.programs.empty()) {
+    const std::size_t bytes = plan.programs.size() * sizeof(ExprInstr);
+    cuda_check(cudaMalloc(&d_sub_prog, bytes), "cudaMalloc(programs)");
+    cuda_check(cudaMemcpy(d_sub_prog, plan.programs.data(), bytes, cudaMemcpyHostToDevice), "cudaMemcpy(programs)");
+    plan.dev.prog = d_sub_prog;
+  }
   cudaStream_t s = stream ? stream : stream_;
   ColPtrs cols;
   bind_columns(plan, ds, cols);
@@ -494,6 +509,10 @@ void Engine::eval_batch(int pdf, const DeviceDataset& ds, const double* theta, d
     cudaEventRecord(ev, s);
     cudaStreamWaitEvent(stream_, ev, 0);
     cudaEventDestroy(ev);
+  }
+  if (d_sub_prog) {
+    cuda_check(cudaStreamSynchronize(s), "eval kernel");
+    cudaFree(d_sub_prog);
   }
 }
 

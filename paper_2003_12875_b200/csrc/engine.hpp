@@ -142,6 +142,7 @@ class Engine {
   NllLaunchInfo last_{};
   GradPlan grad_{};
   std::vector<bool> grad_const_;  // constness the layout was compiled for
+  ExprInstr* d_prog_ = nullptr;  // device copy of plan_.programs
   SumPair* d_gslots_ = nullptr;
   SumPair* h_gslots_ = nullptr;  // pinned
   std::size_t cap_gslots_ = 0;

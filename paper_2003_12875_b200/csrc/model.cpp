@@ -3,6 +3,7 @@
 #include "model.hpp"
 
 #include <charconv>
+#include <algorithm>
 #include <cmath>
 #include <fstream>
 #include <map>
@@ -114,6 +115,7 @@ const char* kind_name(Kind k) {
     case Kind::Chebychev: return "Chebychev";
     case Kind::Polynomial: return "Polynomial";
     case Kind::ProdPdf: return "ProdPdf";
+    case Kind::Expression: return "Expression";
   }
   return "?";
 }
@@ -318,8 +320,37 @@ std::unique_ptr<Model> Model::parse(const std::string& text, const std::string& 
         }
         pdf.obs = pdf.children.size() == 1 ? m->pdfs[pdf.children[0]].obs : -1;
       } else if (call.kind == "Expression") {
-        parse_fail(origin, line_no,
-                   "Expression pdfs have no GPU kernel (use ArgusBG, Chebychev, Polynomial, ...)");
+        // Expression("<formula>", v1, ..., vk) (proj/src/model.cpp:218-232): the variables
+        // are the observable and parameters the formula may use, in program-slot order
+        if (call.args.empty()) parse_fail(origin, line_no, "Expression(\"<formula>\", <var>, ...)");
+        pdf.kind = Kind::Expression;
+        std::vector<std::string> vars(call.args.begin() + 1, call.args.end());
+        for (const std::string& v : vars) {
+          const int o = obs_id(v);
+          if (o >= 0) {
+            if (pdf.obs >= 0 && pdf.obs != o) {
+              parse_fail(origin, line_no, "an Expression pdf depends on one observable");
+            }
+            pdf.obs = o;
+            pdf.expr_vars.push_back(-1);
+            continue;
+          }
+          if (!names.count(v)) parse_fail(origin, line_no, "undeclared name: " + v);
+          const int k = param_id(v);
+          pdf.expr_vars.push_back(k);
+          if (std::find(pdf.params.begin(), pdf.params.end(), k) == pdf.params.end()) pdf.params.push_back(k);
+        }
+        if (pdf.obs < 0) {
+          if (m->observables.size() != 1) {
+            parse_fail(origin, line_no, "an Expression pdf must name its observable");
+          }
+          pdf.obs = 0;  // the reference's single model observable
+        }
+        try {
+          pdf.program = std::make_shared<const ExprProgram>(compile_expression(call.args[0], vars));
+        } catch (const Error& e) {
+          parse_fail(origin, line_no, e.what());
+        }
       } else {
         parse_fail(origin, line_no, "unknown pdf kind: " + call.kind);
       }
@@ -478,6 +509,7 @@ std::optional<double> Model::analytic_integral(int id, double lo, double hi,
       return normalization(id, theta);
     case Kind::ChiSquare:
     case Kind::JohnsonSU:
+    case Kind::Expression:
       return std::nullopt;
   }
   return std::nullopt;
@@ -556,6 +588,17 @@ double Model::eval_unnorm_1d(int id, const double* theta, double x) const {
     case Kind::ProdPdf:
       if (p.children.size() == 1) return eval_unnorm_1d(p.children[0], theta, x);
       usage_error("eval_unnorm_1d: multi-observable ProdPdf");
+    case Kind::Expression: {  // PdfSpec::eval_unnorm, proj/src/pdfs.cpp:200-207
+      double small[16];
+      std::vector<double> big;
+      double* v = small;
+      if (p.expr_vars.size() > 16) {
+        big.resize(p.expr_vars.size());
+        v = big.data();
+      }
+      for (std::size_t i = 0; i < p.expr_vars.size(); ++i) v[i] = p.expr_vars[i] < 0 ? x : theta[p.expr_vars[i]];
+      return p.program->eval(v);
+    }
   }
   return 0.0;
 }

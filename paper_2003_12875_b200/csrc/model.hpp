@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "common.hpp"
+#include "expr.hpp"
 
 namespace ffb {
 
@@ -30,6 +31,7 @@ enum class Kind {
   Chebychev,    // (x, a1, ..., an)
   Polynomial,   // (x, a1, ..., an)
   ProdPdf,      // (p1, ..., pk) over independent observables
+  Expression,   // ("formula", v1, ..., vk)      proj/src/model.cpp:218-232, proj/src/expr.cpp
 };
 
 const char* kind_name(Kind k);
@@ -53,6 +55,10 @@ struct Pdf {
   int obs = -1;                // observable index (leaves, sums: the common observable)
   std::vector<int> params;     // leaf parameters, or sum coefficients (fractions / yields)
   std::vector<int> children;   // component / factor pdf indices
+  // Expression: the compiled formula and, per formula variable, the parameter index
+  // or -1 for the observable (params then lists the distinct parameters)
+  std::shared_ptr<const ExprProgram> program;
+  std::vector<int> expr_vars;
 };
 
 class Model {

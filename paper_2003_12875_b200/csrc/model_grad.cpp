@@ -132,6 +132,8 @@ double Model::eval_unnorm_1d_grad(int id, const double* theta, double x, int j) 
     case Kind::ProdPdf:
       if (p.children.size() == 1) return eval_unnorm_1d_grad(p.children[0], theta, x, j);
       usage_error("eval_unnorm_1d_grad: multi-observable ProdPdf");
+    case Kind::Expression:
+      usage_error("Expression pdfs have no analytic derivative");
   }
   return 0.0;
 }

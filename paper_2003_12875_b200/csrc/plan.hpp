@@ -34,7 +34,42 @@ enum LeafKind : int {
   LK_ARGUS = 4,    // c: [coef, m0, c, p, 1/m0]
   LK_CHEB = 5,     // c: [coef, lo+hi, 1/(hi-lo), a1..an]
   LK_POLY = 6,     // c: [coef, a1..an]
+  LK_EXPR = 7,     // c: [coef, v_0..v_{k-1}] (the formula's parameter values); order = program
+                   // offset in DevPlan::prog
 };
+
+// Expression programs (expr.hpp): postfix instructions, END-terminated on the device.
+enum ExprOp : int {
+  EX_CONST = 0,  // push c
+  EX_VAR,        // push variable `slot` (host programs) / constant row entry 1 + slot (device)
+  EX_ADD,
+  EX_SUB,
+  EX_MUL,
+  EX_DIV,
+  EX_NEG,
+  EX_POW,        // general power
+  EX_SQUARE,
+  EX_CUBE,
+  EX_FOURTH,
+  EX_EXP,
+  EX_LOG,
+  EX_SIN,
+  EX_COS,
+  EX_SQRT,
+  EX_ABS,
+  EX_SINH,
+  EX_ASINH,
+  EX_END,
+  EX_X,          // device programs: push the event's observable value
+};
+
+struct ExprInstr {
+  int op;
+  int slot;
+  double c;
+};
+
+constexpr int kExprMaxDepth = 16;  // device interpreter stack
 
 // END_* close the innermost sum / product after this term; BEGIN_SUM marks the
 // first term of a sum, BEGIN_PROD the term that closes the first sum (factor) of a
@@ -55,6 +90,7 @@ struct DevPlan {
   int stride;  // doubles per parameter point
   int simple;  // 1: a single sum of terms (no product structure)
   DevTerm t[kMaxTerms];
+  const ExprInstr* prog;  // device copy of the plan's Expression programs (or null)
 };
 
 // Fused NLL + gradient pass (kernels.cu nll_grad_kernel).  With W_f(x) = the product

@@ -17,6 +17,7 @@ struct Emitter {
   std::vector<double> consts;
   std::vector<int> col_obs;
   std::vector<int> term_pdf;
+  std::vector<ExprInstr> programs;
 
   int slot(int obs) {
     for (std::size_t i = 0; i < col_obs.size(); ++i) {
@@ -90,6 +91,23 @@ struct Emitter {
         t.order = static_cast<int>(p.params.size());
         for (int k = 0; k < t.order; ++k) consts.push_back(par(p, k));
         break;
+      case Kind::Expression: {  // device program: variables -> the event value or the row
+        t.kind = LK_EXPR;
+        if (p.program->max_depth > kExprMaxDepth) {
+          usage_error("Expression '" + p.name + "' needs a stack of " + std::to_string(p.program->max_depth) +
+                      "; the device interpreter holds " + std::to_string(kExprMaxDepth));
+        }
+        t.order = static_cast<int>(programs.size());
+        for (ExprInstr in : p.program->code) {
+          if (in.op == EX_VAR) {
+            if (p.expr_vars[in.slot] < 0) in.op = EX_X;
+          }
+          programs.push_back(in);
+        }
+        programs.push_back(ExprInstr{EX_END, 0, 0.0});
+        for (const int v : p.expr_vars) consts.push_back(v < 0 || !theta ? 0.0 : theta[v]);
+        break;
+      }
       default:
         usage_error("internal: not a leaf");
     }
@@ -167,7 +185,7 @@ struct Emitter {
 }  // namespace
 
 HostPlan compile_plan(const Model& m, int pdf, bool normalized) {
-  Emitter e{m, nullptr, {}, {}, {}, {}};
+  Emitter e{m, nullptr, {}, {}, {}, {}, {}};
   e.root(pdf, 1.0);
   if (e.terms.size() > static_cast<std::size_t>(kMaxTerms)) {
     usage_error("model has " + std::to_string(e.terms.size()) + " leaf terms; the GPU plan holds " +
@@ -181,6 +199,8 @@ HostPlan compile_plan(const Model& m, int pdf, bool normalized) {
   hp.normalized = normalized;
   hp.col_obs = e.col_obs;
   hp.term_pdf = e.term_pdf;
+  hp.programs = e.programs;
+  hp.dev.prog = nullptr;  // the engine points this at its device copy
   hp.dev.nterms = static_cast<int>(e.terms.size());
   hp.dev.ncols = static_cast<int>(e.col_obs.size());
   hp.dev.stride = static_cast<int>(e.consts.size());
@@ -214,7 +234,7 @@ void build_constants(const HostPlan& plan, const Model& m, const double* theta, 
   m.check_params(plan.pdf, theta);
   const double scale =
       (plan.normalized ? 1.0 / m.normalization(plan.pdf, theta) : 1.0) * extra_scale;
-  Emitter e{m, theta, {}, {}, {}, {}};
+  Emitter e{m, theta, {}, {}, {}, {}, {}};
   e.root(plan.pdf, scale);
   if (static_cast<int>(e.consts.size()) != plan.dev.stride) usage_error("internal: plan drift");
   for (int i = 0; i < plan.dev.stride; ++i) row[i] = e.consts[i];
@@ -331,7 +351,11 @@ GradPlan compile_grad_plan(const HostPlan& plan, const Model& m) {
   }
   gp.dev.nslots = slot;
   gp.dev.nfactors = factor;
-  if (slot > kMaxGradSlots) {
+  bool has_expr = false;
+  for (int i = 0; i < d.nterms; ++i) has_expr = has_expr || d.t[i].kind == LK_EXPR;
+  if (has_expr) {
+    gp.why = "Expression pdfs have no analytic derivative (use finite differences)";
+  } else if (slot > kMaxGradSlots) {
     gp.why = "gradient layout needs " + std::to_string(slot) + " accumulators; the device pass holds " +
              std::to_string(kMaxGradSlots);
   } else if (factor > kMaxFactors) {

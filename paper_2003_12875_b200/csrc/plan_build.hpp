@@ -17,6 +17,7 @@ struct HostPlan {
   bool normalized = true;  // true: p = unnorm / N (the likelihood); false: eval_batch
   std::vector<int> col_obs;  // compact column slot -> observable index
   std::vector<int> term_pdf; // leaf pdf of each term
+  std::vector<ExprInstr> programs;  // Expression leaves' device programs (DevPlan::prog)
 };
 
 // Slot layout of the fused NLL + gradient pass (plan.hpp DevGradPlan) for the

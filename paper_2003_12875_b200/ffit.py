@@ -484,3 +484,18 @@ def sample_host(model: Model, n: int, seed: int):
     eff = ctypes.c_double()
     _check(lib().ffcu_sample_host(model.handle, n, seed, cp, ctypes.byref(eff)))
     return dict(zip(names, cols)), eff.value
+
+
+def expr_eval(text: str, variables, values) -> np.ndarray:
+    """The Expression formula language on the host: compile `text` over `variables` and
+    evaluate it at rows of values (npts x nvars) -- the per-event semantics the device
+    interpreter follows (proj/docs/expression-grammar.md)."""
+    vals = np.asarray(values, dtype=np.float64)
+    if vals.ndim == 1:
+        vals = vals[None, :]
+    npts = vals.shape[0]
+    buf = _f64(vals.reshape(-1)) if vals.size else np.zeros(1)
+    arr = (CP * max(len(variables), 1))(*[v.encode() for v in variables])
+    out = np.empty(max(npts, 1))
+    _check(lib().ffcu_expr_eval(text.encode(), arr, len(variables), _dp(buf), npts, _dp(out)))
+    return out[:npts]

@@ -471,3 +471,67 @@ def test_streaming_ragged_sizes(n):
     _, comp, _ = o.nll(cols)
     assert abs(v.value - comp) <= NLL_TOL * abs(comp)
     assert v.first_invalid == -1
+
+
+# ------------------------------------------------------------------ Expression pdfs (f4)
+
+@pytest.mark.parametrize("name", list(EXPR_MODELS))
+def test_expression_pdfs_run_the_reference_text_on_the_gpu(name):
+    """The reference's OWN Expression model text (e.g. ArgusBG spelled as a formula) on the
+    device interpreter vs the reference's per-event values and NLL (golden)."""
+    ref_text, _, _, col = EXPR_MODELS[name]
+    g = np.load(os.path.join(GOLD, "expr_models.npz"))
+    x, p, sc = g[f"{name}/x"], g[f"{name}/p"], g[f"{name}/scalars"]
+    m = fb.Model.from_string(ref_text)
+    ds = fb.DataSet.from_columns({col: x})
+    assert rel(fb.probabilities(m, ds), p) <= PER_EVENT
+    assert abs(fb.nll(m, ds).value - sc[0]) <= NLL_TOL * abs(sc[0])
+    many, _, _ = fb.nll_points(m, ds, np.repeat(m.theta()[None, :], 10, axis=0))  # tile kernel
+    assert np.all(np.abs(many - sc[0]) <= NLL_TOL * abs(sc[0]))
+
+
+def test_expression_config2_reference_text_matches_reference_engine():
+    """BASELINE config 2 exactly as the reference spells it (configs.REFERENCE_TEXTS: the
+    ArgusBG as an Expression) against the unmodified reference engine at several points."""
+    from oracle.oracle import RefDataset, RefModel, ref_available
+    if not ref_available():
+        pytest.skip("oracle/_ref not built")
+    w = configs.C2
+    text = configs.REFERENCE_TEXTS[w.name]
+    m = fb.Model.from_string(text)
+    cols, _ = fb.sample_host(fb.Model.from_string(w.text), 30_011, 5)
+    ds = fb.DataSet.from_columns(cols)
+    r = RefModel(text)
+    rds = RefDataset("x", cols["x"])
+    pts = w.points(m, n_points=3)
+    vals, _, _ = fb.nll_points(m, ds, pts)
+    for p in range(3):
+        for name, v in zip(m.param_names, pts[p]):
+            if not m.is_constant(name):
+                r.set(name, v)
+        want = r.nll_compensated(rds)[0]
+        assert abs(vals[p] - want) <= NLL_TOL * abs(want)
+
+
+def test_expression_sub_pdf_eval_batch_and_invalid_events():
+    """eval_batch of an Expression sub-pdf (its own uploaded program) against the host
+    interpreter; a formula that is negative somewhere flags those events invalid."""
+    text = EXPR_MODELS["argus_mix"][0]
+    m = fb.Model.from_string(text)
+    x = np.linspace(5.2, 5.29, 5001)
+    ds = fb.DataSet.from_columns({"x": x})
+    got = fb.eval_batch(m, "bkg", ds)
+    want = fb.expr_eval("x*sqrt(1-(x/m0)^2)*exp(c*(1-(x/m0)^2))", ["x", "m0", "c"],
+                        np.column_stack([x, np.full_like(x, 5.291), np.full_like(x, -20.0)]))
+    assert rel(got, want) <= PER_EVENT
+    bad = fb.Model.from_string("observable x -1 1\nparameter a 0.5 0 1\npdf e Expression(\"a + x\", x, a)\n")
+    v = fb.nll(bad, fb.DataSet.from_columns({"x": np.array([0.1, 0.2, -0.7, 0.3])}))
+    assert v.value == np.inf and v.first_invalid == 2
+
+
+def test_expression_fit_uses_finite_differences():
+    text = EXPR_MODELS["argus_mix"][0]
+    m = fb.Model.from_string(text)
+    cols, _ = fb.sample_host(m, 20_000, 3)
+    r = fb.fit_gradient(m, fb.DataSet.from_columns(cols), tolerance=1e-10, max_iterations=200)
+    assert r.converged and not r.analytic_gradient
