@@ -66,9 +66,9 @@ def test_parse_errors_use_reference_codes():
     with pytest.raises(fb.FfitError) as e:
         fb.Model.from_string("observable x 0 1\nparameter a 5 0 2\n")
     assert e.value.code == 1  # value outside range: Graph::add_parameter, Usage
-    with pytest.raises(fb.FfitError) as e:
-        fb.Model.from_string('observable x 0 1\nparameter a 1 0 2\npdf e Expression("a*x", x, a)\n')
-    assert e.value.code == 2 and "no GPU kernel" in e.value.message
+    with pytest.raises(fb.FfitError) as e:  # formula errors become model-file parse errors
+        fb.Model.from_string('observable x 0 1\nparameter a 1 0 2\npdf e Expression("a*x+", x, a)\n')
+    assert e.value.code == 2 and "syntax error at offset 4" in e.value.message
     with pytest.raises(fb.FfitError) as e:
         fb.Model.from_string("observable x 0 1\nparameter a 1 0 2\n")
     assert e.value.code == 2 and "no pdf" in e.value.message
