@@ -180,6 +180,11 @@ def run_ours(args, w):
     model = fb.Model.from_string(w.text)
     n = args.events or w.n_events
     cols, _ = fb.sample_host(model, n, shard_seed(w, rank))
+    if args.spelling == "reference":
+        # the reference's own model text (C2: ArgusBG as an Expression pdf) through the
+        # device Expression interpreter, on the same events
+        from paper_2003_12875_b200 import configs as _cfg
+        model = fb.Model.from_string(_cfg.REFERENCE_TEXTS[w.name])
     names = model.observables
     ds = fb.DataSet.from_columns(cols)
     pts = w.points(model, n_points=args.points)
@@ -290,7 +295,7 @@ def run_ours(args, w):
         "config": {"workload": w.name, "description": w.description, "events_per_gpu": n, "points_per_launch": P,
                    "l2": "flushed between timed steps (512 MiB write)",
                    "parallelism": f"event shards x{world}" + (", NCCL all_gather of 2P doubles" if coll else ""),
-                   "launch": info},
+                   "launch": info, "spelling": args.spelling},
         "roofline": roofline, "e2e": e2e, "clocks": clk, "gpu_launches": int(launches),
         "result_finite": ok,
     }
@@ -459,6 +464,8 @@ def main():
     ap.add_argument("--force-collective", action="store_true",
                     help="run the NCCL all-gather + combine exchange even at N = 1")
     ap.add_argument("--iterations", type=int, default=50, help="fit iterations (--fit / c5)")
+    ap.add_argument("--spelling", default="ours", choices=["ours", "reference"],
+                    help="model text: ours (ArgusBG kind) or the reference's (Expression pdf)")
     ap.add_argument("--gradient", default="fd", choices=["fd", "analytic"],
                     help="c5 fit gradients: central differences (the config's 2d+1 points per launch) "
                          "or the fused NLL + gradient pass")
