@@ -125,6 +125,21 @@ const char* ffcu_dataset_column_name(const ffit_dataset* ds, int i);
 int ffcu_dataset_download(const ffit_dataset* ds, int col, double* host_out);
 int ffcu_dataset_device_column(const ffit_dataset* ds, int col, const double** dev_ptr);
 
+/* Binary SoA dataset files (the reference's only on-disk format is
+ * CSV, proj/src/dataset.cpp:61-146).  `.ffsoa` = the HBM layout on disk: a 4 KiB-aligned
+ * header (magic, column names, per-column checksums) then each fp64 column contiguous and
+ * 4 KiB-aligned (csrc/soa_io.hpp).  Loading reads chunks into two pinned staging buffers,
+ * each chunk's host-to-device copy overlapping the read of the next; checksums are
+ * verified (FFIT_ERR_DATA on mismatch, truncation or a bad header). */
+int ffcu_soa_write(const char* path, const char* const* names, const double* const* cols, int ncols,
+                   long long n);
+int ffcu_dataset_save_soa(const ffit_dataset* ds, const char* path);
+int ffcu_dataset_load_soa(const char* path, ffit_dataset** out, double* seconds);
+int ffcu_soa_info(const char* path, int* ncols, long long* nrows);
+int ffcu_soa_column_name(const char* path, int col, char* buf, int cap);
+/* Host read of every column (cols[i]: nrows doubles each), checksums verified. */
+int ffcu_soa_read_host(const char* path, double* const* cols);
+
 /* NLL at P parameter points in ONE launch.  points: P x ffit_model_param_count
  * doubles, row-major, parameters in ffit_model_param_name order.  values[p]
  * = NLL (+inf if an event has p <= 0 or non-finite; first_invalid[p] = its

@@ -9,4 +9,4 @@ from .ffit import (  # noqa: F401
     DataSet, EvalMode, FfitError, FitResult, Model, NllValue, eval_batch, expr_eval, fit_gradient, fit_to,
     fp64_peak, kernel_launches, kernel_timer, kernel_timer_read, last_launch, nll, nll_c, nll_points,
     nll_points_device, nll_grad, nll_grad_finish, nll_grad_partial, grad_slot_count,
-    nll_points_partial, normalization, probabilities, sample_host)
+    nll_points_partial, normalization, probabilities, read_soa_host, sample_host, write_soa)

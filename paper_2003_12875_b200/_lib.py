@@ -85,6 +85,12 @@ SIGNATURES = {
     "ffcu_point_constants": (I, [VP, DP, DP]),
     "ffcu_coef_derivatives": (I, [VP, DP, I, DP]),
     "ffcu_expr_eval": (I, [CP, ctypes.POINTER(CP), I, DP, I, DP]),
+    "ffcu_soa_write": (I, [CP, ctypes.POINTER(CP), ctypes.POINTER(DP), I, LL]),
+    "ffcu_dataset_save_soa": (I, [VP, CP]),
+    "ffcu_dataset_load_soa": (I, [CP, ctypes.POINTER(VP), ctypes.POINTER(D)]),
+    "ffcu_soa_info": (I, [CP, IP, ctypes.POINTER(LL)]),
+    "ffcu_soa_column_name": (I, [CP, I, CP, I]),
+    "ffcu_soa_read_host": (I, [CP, ctypes.POINTER(DP)]),
     "ffcu_model_pdf_count": (I, [VP]),
     "ffcu_model_pdf_name": (CP, [VP, I]),
     "ffcu_model_observable_count": (I, [VP]),

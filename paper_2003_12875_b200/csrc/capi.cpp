@@ -14,6 +14,7 @@
 #include "engine.hpp"
 #include "fit.hpp"
 #include "sampler.hpp"
+#include "soa_io.hpp"
 
 #define FFB_API extern "C" __attribute__((visibility("default")))
 
@@ -639,6 +640,86 @@ FFB_API int ffcu_dataset_from_host(const char* const* names, const double* const
       c.push_back(n > 0 ? cols[i] : nullptr);
     }
     *out = new ffit_dataset{ffb::DeviceDataset::upload(nm, c, n)};
+  });
+}
+
+FFB_API int ffcu_soa_write(const char* path, const char* const* names, const double* const* cols, int ncols,
+                           long long n) {
+  return guarded([&] {
+    require(path, "path");
+    require(names, "names");
+    if (ncols <= 0) ffb::usage_error("a dataset needs at least one column");
+    if (n > 0) require(cols, "cols");
+    std::vector<std::string> nm;
+    std::vector<const double*> c;
+    for (int i = 0; i < ncols; ++i) {
+      require(names[i], "names[i]");
+      nm.push_back(names[i]);
+      c.push_back(n > 0 ? cols[i] : nullptr);
+    }
+    ffb::soa_write(path, nm, c, n);
+  });
+}
+
+FFB_API int ffcu_dataset_save_soa(const ffit_dataset* ds, const char* path) {
+  return guarded([&] {
+    require(ds, "dataset");
+    require(path, "path");
+    const ffb::DeviceDataset& d = *ds->d;
+    std::vector<std::vector<double>> host(d.cols.size(), std::vector<double>(static_cast<std::size_t>(d.n)));
+    std::vector<const double*> c;
+    for (std::size_t i = 0; i < d.cols.size(); ++i) {
+      if (d.n > 0) d.download(static_cast<int>(i), host[i].data());
+      c.push_back(host[i].data());
+    }
+    ffb::soa_write(path, d.names, c, d.n);
+  });
+}
+
+FFB_API int ffcu_dataset_load_soa(const char* path, ffit_dataset** out, double* seconds) {
+  return guarded([&] {
+    require(path, "path");
+    require(out, "out");
+    ffb::SoaLoadStats st;
+    auto d = ffb::soa_load_device(path, &st);
+    if (seconds) *seconds = st.seconds;
+    *out = new ffit_dataset{std::move(d)};
+  });
+}
+
+FFB_API int ffcu_soa_info(const char* path, int* ncols, long long* nrows) {
+  return guarded([&] {
+    require(path, "path");
+    const ffb::SoaHeader h = ffb::soa_read_header(path);
+    if (ncols) *ncols = static_cast<int>(h.names.size());
+    if (nrows) *nrows = h.nrows;
+  });
+}
+
+FFB_API int ffcu_soa_column_name(const char* path, int col, char* buf, int cap) {
+  return guarded([&] {
+    require(path, "path");
+    require(buf, "buf");
+    const ffb::SoaHeader h = ffb::soa_read_header(path);
+    if (col < 0 || col >= static_cast<int>(h.names.size())) ffb::usage_error("column index out of range");
+    const std::string& s = h.names[col];
+    if (cap < static_cast<int>(s.size()) + 1) ffb::usage_error("buffer too small");
+    std::memcpy(buf, s.c_str(), s.size() + 1);
+  });
+}
+
+FFB_API int ffcu_soa_read_host(const char* path, double* const* cols) {
+  return guarded([&] {
+    require(path, "path");
+    require(cols, "cols");
+    ffb::SoaHeader h;
+    const auto data = ffb::soa_read_host(path, &h);
+    for (std::size_t c = 0; c < data.size(); ++c) {
+      if (h.nrows > 0) {
+        require(cols[c], "cols[c]");
+        std::memcpy(cols[c], data[c].data(), static_cast<std::size_t>(h.nrows) * sizeof(double));
+      }
+    }
   });
 }
 

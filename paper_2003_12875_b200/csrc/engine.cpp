@@ -89,6 +89,12 @@ std::shared_ptr<DeviceDataset> DeviceDataset::upload(const std::vector<std::stri
                                                      const std::vector<const double*>& host_cols,
                                                      long long n) {
   if (names.size() != host_cols.size()) usage_error("dataset: names/columns length mismatch");
+  auto ds = allocate(names, n);
+  ds->copy_from_host(host_cols);
+  return ds;
+}
+
+std::shared_ptr<DeviceDataset> DeviceDataset::allocate(const std::vector<std::string>& names, long long n) {
   if (n < 0) usage_error("dataset: negative row count");
   for (std::size_t i = 0; i < names.size(); ++i) {
     for (std::size_t j = 0; j < i; ++j) {
@@ -107,7 +113,6 @@ std::shared_ptr<DeviceDataset> DeviceDataset::upload(const std::vector<std::stri
     cuda_check(cudaMalloc(&d, static_cast<std::size_t>(padded) * sizeof(double)), "cudaMalloc(column)");
     ds->cols.push_back(d);
   }
-  ds->copy_from_host(host_cols);
   return ds;
 }
 

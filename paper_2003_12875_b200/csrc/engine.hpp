@@ -34,6 +34,8 @@ struct DeviceDataset {
 
   int column_index(const std::string& name) const;  // -1 if absent
 
+  // Owned, uninitialised columns of n rows (padded to whole 2048-event tiles).
+  static std::shared_ptr<DeviceDataset> allocate(const std::vector<std::string>& names, long long n);
   static std::shared_ptr<DeviceDataset> upload(const std::vector<std::string>& names,
                                                const std::vector<const double*>& host_cols,
                                                long long n);

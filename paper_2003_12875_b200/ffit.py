@@ -184,6 +184,18 @@ class DataSet:
         return cls(h, keep=tensors)
 
     @classmethod
+    def load_soa(cls, path: str):
+        """HBM dataset from an .ffsoa file (pinned, chunked, overlapped upload).  Returns
+        (dataset, seconds)."""
+        h = VP()
+        sec = ctypes.c_double()
+        _check(lib().ffcu_dataset_load_soa(str(path).encode(), ctypes.byref(h), ctypes.byref(sec)))
+        return cls(h), sec.value
+
+    def save_soa(self, path: str):
+        _check(lib().ffcu_dataset_save_soa(self._h, str(path).encode()))
+
+    @classmethod
     def sample(cls, model: Model, n: int, seed: int):
         h = VP()
         eff = ctypes.c_double()
@@ -499,3 +511,30 @@ def expr_eval(text: str, variables, values) -> np.ndarray:
     out = np.empty(max(npts, 1))
     _check(lib().ffcu_expr_eval(text.encode(), arr, len(variables), _dp(buf), npts, _dp(out)))
     return out[:npts]
+
+
+def write_soa(path: str, columns: dict):
+    """Write host columns (name -> 1-D float64 array) as an .ffsoa file."""
+    names = list(columns)
+    cols = [_f64(columns[n]) for n in names]
+    n = len(cols[0]) if cols else 0
+    if any(len(c) != n for c in cols):
+        raise FfitError(USAGE, "columns have unequal lengths")
+    cn = (CP * len(names))(*[s.encode() for s in names])
+    cp = (DP * len(cols))(*[_dp(c) for c in cols])
+    _check(lib().ffcu_soa_write(str(path).encode(), cn, cp, len(names), n))
+
+
+def read_soa_host(path: str) -> dict:
+    """Host columns of an .ffsoa file (checksums verified)."""
+    nc, nr = ctypes.c_int(), LL()
+    _check(lib().ffcu_soa_info(str(path).encode(), ctypes.byref(nc), ctypes.byref(nr)))
+    names = []
+    for i in range(nc.value):
+        buf = ctypes.create_string_buffer(4096)
+        _check(lib().ffcu_soa_column_name(str(path).encode(), i, buf, 4096))
+        names.append(buf.value.decode())
+    cols = [np.empty(nr.value) for _ in names]
+    cp = (DP * len(cols))(*[_dp(c) if c.size else _dp(np.empty(1)) for c in cols])
+    _check(lib().ffcu_soa_read_host(str(path).encode(), cp))
+    return dict(zip(names, cols))
