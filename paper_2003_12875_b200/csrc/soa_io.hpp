@@ -46,9 +46,10 @@ struct SoaLoadStats {
   std::uint64_t bytes = 0;
 };
 
-// Loads straight into a new HBM-resident dataset on the current device: chunked reads
-// into two pinned staging buffers, each chunk's cudaMemcpyAsync overlapping the read of
-// the next; checksums verified on the host while the copies fly.
+// Loads straight into a new HBM-resident dataset on the current device: 16 MiB chunks
+// spread over four reader threads, each with two pinned staging buffers and its own
+// stream, so that every chunk's cudaMemcpyAsync overlaps the next read; checksums are
+// accumulated while the copies fly and verified at the end.
 std::shared_ptr<DeviceDataset> soa_load_device(const std::string& path, SoaLoadStats* stats);
 
 std::uint64_t soa_checksum(const double* col, long long n);
