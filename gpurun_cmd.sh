@@ -1,11 +1,8 @@
-python -m pytest tests -m gpu -q 2>&1 | tail -2 > gpurun_out/pytest_gpu.log
-mkdir -p gpurun_out/v10
-for w in c2 c1 c3 c4; do
-  python bench.py --workload $w --steps 20 > gpurun_out/v10/bench_$w.json 2>> gpurun_out/v10/err.log
+python -m pytest tests/test_gpu_parity.py -q -x 2>&1 | tail -2
+for rep in 1 2; do
+for tag in base gv1; do
+  if [ $tag = base ]; then unset FFB_LIB_VARIANT; else export FFB_LIB_VARIANT=$tag; fi
+  python bench.py --workload c3 --no-cpu-baseline --steps 20 > gpurun_out/ab.json 2>> gpurun_out/ab_err.log
+  python -c "import json;d=json.load(open('gpurun_out/ab.json'));print('c3 $tag', '%.4e'%d['value'])"
 done
-python bench.py --workload c5 --gradient fd > gpurun_out/v10/bench_c5_fd.json 2>> gpurun_out/v10/err.log
-python bench.py --workload c5 --gradient analytic > gpurun_out/v10/bench_c5_analytic.json 2>> gpurun_out/v10/err.log
-python tools/small_p_bench.py > gpurun_out/v10/small_p.txt 2>&1
-python tools/grad_bench.py > gpurun_out/v10/grad_bench.txt 2>&1
-python bench.py > gpurun_out/v10/bench_default.json 2>> gpurun_out/v10/err.log
-cat gpurun_out/pytest_gpu.log
+done
