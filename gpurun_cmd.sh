@@ -1,4 +1,3 @@
-for tag in base wt gb3 both; do
-  if [ $tag = base ]; then unset FFB_LIB_VARIANT; else export FFB_LIB_VARIANT=$tag; fi
-  echo "== $tag"; python tools/grad_bench.py 2>&1 | cut -c1-80
-done
+python bench.py > gpurun_out/default.json 2> gpurun_out/default.err; echo "ours rc=$?"
+python bench.py --impl reference > gpurun_out/ref.json 2> gpurun_out/ref.err; echo "ref rc=$?"
+cat gpurun_out/default.json; echo; cat gpurun_out/ref.json
