@@ -1,3 +1,4 @@
-python bench.py > gpurun_out/default.json 2> gpurun_out/default.err; echo "ours rc=$?"
-python bench.py --impl reference > gpurun_out/ref.json 2> gpurun_out/ref.err; echo "ref rc=$?"
-cat gpurun_out/default.json; echo; cat gpurun_out/ref.json
+for tag in base ge8 ge2; do
+  if [ $tag = base ]; then unset FFB_LIB_VARIANT; else export FFB_LIB_VARIANT=$tag; fi
+  echo "== $tag"; python tools/grad_bench.py 2>&1 | cut -c1-80
+done
