@@ -179,7 +179,21 @@ def run_ours(args, w):
 
     model = fb.Model.from_string(w.text)
     n = args.events or w.n_events
-    cols, _ = fb.sample_host(model, n, shard_seed(w, rank))
+    load_s = None
+    if args.inputs:
+        # tools/make_inputs.py output: the same seeded events, from disk through the
+        # pinned overlapped .ffsoa upload (its time reported as config.inputs_load_s)
+        import json as _json
+        stem = os.path.join(args.inputs, w.name + (f".r{rank}" if rank else ""))
+        man = _json.load(open(stem + ".json"))
+        if man["seed"] != shard_seed(w, rank) or (args.events and man["n"] != n):
+            raise SystemExit(f"{stem}.json does not match this run (seed/events)")
+        n = man["n"]
+        ds_disk, load_s = fb.DataSet.load_soa(stem + ".ffsoa")
+        cols = {k: ds_disk.column(k) for k in man["columns"]}
+        del ds_disk
+    else:
+        cols, _ = fb.sample_host(model, n, shard_seed(w, rank))
     if args.spelling == "reference":
         # the reference's own model text (C2: ArgusBG as an Expression pdf) through the
         # device Expression interpreter, on the same events
@@ -295,7 +309,8 @@ def run_ours(args, w):
         "config": {"workload": w.name, "description": w.description, "events_per_gpu": n, "points_per_launch": P,
                    "l2": "flushed between timed steps (512 MiB write)",
                    "parallelism": f"event shards x{world}" + (", NCCL all_gather of 2P doubles" if coll else ""),
-                   "launch": info, "spelling": args.spelling},
+                   "launch": info, "spelling": args.spelling,
+                   "inputs": args.inputs or "generated in-process (seeded)", "inputs_load_s": load_s},
         "roofline": roofline, "e2e": e2e, "clocks": clk, "gpu_launches": int(launches),
         "result_finite": ok,
     }
@@ -464,6 +479,7 @@ def main():
     ap.add_argument("--force-collective", action="store_true",
                     help="run the NCCL all-gather + combine exchange even at N = 1")
     ap.add_argument("--iterations", type=int, default=50, help="fit iterations (--fit / c5)")
+    ap.add_argument("--inputs", default="", help="directory of tools/make_inputs.py files (.ffsoa + manifest)")
     ap.add_argument("--spelling", default="ours", choices=["ours", "reference"],
                     help="model text: ours (ArgusBG kind) or the reference's (Expression pdf)")
     ap.add_argument("--gradient", default="fd", choices=["fd", "analytic"],

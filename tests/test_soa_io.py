@@ -99,3 +99,22 @@ def test_device_load_detects_corruption(tmp_path):
     with pytest.raises(fb.FfitError) as e:
         fb.DataSet.load_soa(p)
     assert e.value.code == 2 and "checksum" in str(e.value)
+
+
+def test_make_inputs_manifest(tmp_path):
+    """tools/make_inputs.py: the generator's columns on disk with seed, N and sha256."""
+    import hashlib
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.run([sys.executable, os.path.join(root, "tools", "make_inputs.py"), "--workload", "c2",
+                    "--events", "20000", "--out", str(tmp_path)], check=True, capture_output=True)
+    man = json.load(open(tmp_path / "c2_gauss_argus_1e7.json"))
+    raw = open(tmp_path / man["file"], "rb").read()
+    assert hashlib.sha256(raw).hexdigest() == man["sha256"]
+    from paper_2003_12875_b200 import configs
+    want, _ = fb.sample_host(fb.Model.from_string(configs.C2.text), 20000, configs.C2.data_seed)
+    got = fb.read_soa_host(tmp_path / man["file"])
+    assert man["seed"] == configs.C2.data_seed and man["n"] == 20000
+    assert got["x"].tobytes() == want["x"].tobytes()
