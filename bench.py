@@ -127,14 +127,19 @@ def peaks():
         return {}
 
 
-def profiled_traffic(workload):
-    """dram bytes per fused-kernel launch from the committed ncu --set full capture."""
+def profiled(workload, key):
+    """A figure of the committed ncu --set full capture (profiles/ncu_summary.json)."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as fh:
             d = json.load(fh)
-        return d.get(workload, {}).get("dram_bytes_per_launch")
+        return d.get(workload, {}).get(key)
     except (OSError, ValueError):
         return None
+
+
+def profiled_traffic(workload):
+    """dram bytes per fused-kernel launch from the committed ncu --set full capture."""
+    return profiled(workload, "dram_bytes_per_launch")
 
 
 def shard_seed(w, rank):
@@ -300,6 +305,9 @@ def run_ours(args, w):
         "hbm_achieved_gbs": n * w.bytes_per_event * info["nchunks"] / (avg_kernel_ms / 1e3) / 1e9,
         "hbm_peak_gbs": peaks().get("hbm_gbs"),
         "traffic": profiled_traffic(w.name),
+        # the same kernel's measured FP64-pipe busy fraction (ncu), beside the work-model frac
+        "ncu_fp64_pipe_active": profiled(w.name, "fp64_pipe_active"),
+        "ncu_source": profiled(w.name, "source"),
     }
 
     line = {
