@@ -205,6 +205,17 @@ int ffcu_coef_derivatives(const ffit_model* m, const double* point, int param, d
  * syntax / unknown identifier / unknown function / arity errors. */
 int ffcu_expr_eval(const char* text, const char* const* vars, int nvars, const double* values, int npts,
                    double* out);
+/* Formula-specialised likelihood builds for models with Expression pdfs: each formula
+ * becomes straight-line device code and the fused kernels are compiled around it at run
+ * time with NVRTC (csrc/jit.cpp), else the device interpreter runs.  enable: 1 on, 0 off,
+ * -1 query; returns the previous setting (default on; FFB_NO_EXPR_JIT=1 turns it off). */
+int ffcu_expression_jit(int enable);
+const char* ffcu_expression_jit_status(void);
+/* The generated formula source of a model (compile = 1: also NVRTC-compile the kernels
+ * around it, no GPU needed); at most cap-1 characters into buf. */
+int ffcu_expression_jit_source(const ffit_model* m, int compile, char* buf, int cap);
+/* 1 if the model's last likelihood launch ran the formula-specialised build. */
+int ffcu_last_launch_jit(const ffit_model* m);
 int ffcu_model_pdf_count(const ffit_model* m);
 const char* ffcu_model_pdf_name(const ffit_model* m, int i);
 int ffcu_model_observable_count(const ffit_model* m);

@@ -85,6 +85,10 @@ SIGNATURES = {
     "ffcu_point_constants": (I, [VP, DP, DP]),
     "ffcu_coef_derivatives": (I, [VP, DP, I, DP]),
     "ffcu_expr_eval": (I, [CP, ctypes.POINTER(CP), I, DP, I, DP]),
+    "ffcu_expression_jit": (I, [I]),
+    "ffcu_expression_jit_status": (CP, []),
+    "ffcu_expression_jit_source": (I, [VP, I, CP, I]),
+    "ffcu_last_launch_jit": (I, [VP]),
     "ffcu_soa_write": (I, [CP, ctypes.POINTER(CP), ctypes.POINTER(DP), I, LL]),
     "ffcu_dataset_save_soa": (I, [VP, CP]),
     "ffcu_dataset_load_soa": (I, [CP, ctypes.POINTER(VP), ctypes.POINTER(D)]),

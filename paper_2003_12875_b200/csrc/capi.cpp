@@ -13,6 +13,7 @@
 
 #include "engine.hpp"
 #include "fit.hpp"
+#include "jit.hpp"
 #include "sampler.hpp"
 #include "soa_io.hpp"
 
@@ -605,6 +606,41 @@ FFB_API int ffcu_expr_eval(const char* text, const char* const* vars, int nvars,
     for (int i = 0; i < npts; ++i) out[i] = prog.eval(values + static_cast<std::size_t>(i) * nvars);
   });
 }
+
+FFB_API int ffcu_expression_jit(int enable) {
+  const int was = ffb::jit_enabled() ? 1 : 0;
+  if (enable >= 0) ffb::jit_enable(enable != 0);
+  return was;
+}
+
+FFB_API const char* ffcu_expression_jit_status(void) {
+  thread_local std::string s;
+  s = ffb::jit_status();
+  return s.c_str();
+}
+
+FFB_API int ffcu_expression_jit_source(const ffit_model* m, int compile, char* buf, int cap) {
+  return guarded([&] {
+    require(m, "model");
+    const ffb::HostPlan& plan = m->engine->likelihood_plan();
+    if (plan.programs.empty()) ffb::usage_error("the model has no Expression pdf");
+    const std::string src = ffb::jit_expression_source(plan);
+    std::string text = src;
+    if (compile) {
+      std::string log;
+      if (!ffb::jit_compile_only(plan, &log)) {
+        ffb::numeric_error("NVRTC compile of the formula-specialised kernels failed: " + log.substr(0, 4000));
+      }
+    }
+    if (buf && cap > 0) {
+      const std::size_t k = std::min<std::size_t>(text.size(), static_cast<std::size_t>(cap - 1));
+      std::memcpy(buf, text.data(), k);
+      buf[k] = '\0';
+    }
+  });
+}
+
+FFB_API int ffcu_last_launch_jit(const ffit_model* m) { return m && m->engine->last_launch().jit ? 1 : 0; }
 
 FFB_API int ffcu_model_pdf_count(const ffit_model* m) { return static_cast<int>(m->m->pdfs.size()); }
 

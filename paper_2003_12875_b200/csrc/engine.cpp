@@ -1,5 +1,7 @@
 #include "engine.hpp"
 
+#include "jit.hpp"
+
 #include <algorithm>
 #include <atomic>
 #include <cmath>
@@ -297,7 +299,12 @@ int Engine::nll_points_device(const DeviceDataset& ds, const double* thetas, int
       }
     }
     const int ks = plan_kind_set(plan_.dev, h_consts_[slot_], P);
-    last_ = launch_nll(plan_.dev, cols, ds.n, d_consts, P, d_scratch_, d_pairs, d_bad, s, ks, ea, eb);
+    if (!plan_.programs.empty() && jit_prepare(plan_)) {
+      // Expression leaves: the formula-specialised build (jit.cpp) instead of the interpreter
+      last_ = launch_nll_jit(plan_, cols, ds.n, d_consts, P, d_scratch_, d_pairs, d_bad, s, ea, eb);
+    } else {
+      last_ = launch_nll(plan_.dev, cols, ds.n, d_consts, P, d_scratch_, d_pairs, d_bad, s, ks, ea, eb);
+    }
     launches = last_.launches;
     cuda_check(cudaGetLastError(), "launch_nll");
   }

@@ -1,0 +1,46 @@
+// Formula-specialised builds of the likelihood kernels for plans with Expression leaves
+// (second stage).  The device interpreter (kernels_device.cuh
+// expr_eval) runs any formula but pays a local-memory stack and an opcode switch per
+// operation; here each formula of the plan becomes straight-line device code
+// (`ffb_expr_batch`), the fused kernels of kernels_device.cuh are compiled around it at
+// run time with NVRTC (sm_100a SASS), loaded through the driver API and launched with the
+// same shapes as the static builds.  Modules are cached per (device, source).
+//
+// NVRTC and the driver are reached through dlopen / cudaGetDriverEntryPoint, so the
+// library has no link-time dependency on either; when NVRTC is absent or a compile fails
+// the engine keeps the interpreter (jit_status() says why).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "kernels.cuh"
+#include "plan_build.hpp"
+
+namespace ffb {
+
+// The generated formula functions for `plan` (prepended to kernels_device.cuh).
+std::string jit_expression_source(const HostPlan& plan);
+
+// Whether the JIT path is switched on (default: on; FFB_NO_EXPR_JIT=1 or
+// ffcu_expression_jit(0) turns it off).
+bool jit_enabled();
+void jit_enable(bool on);
+
+// Compiles (or fetches from the cache) the kernels for `plan` on the current device;
+// false (with the reason in jit_status()) when that is not possible.
+bool jit_prepare(const HostPlan& plan);
+std::string jit_status();
+
+// As launch_nll, through the plan's formula-specialised kernels (jit_prepare first).
+NllLaunchInfo launch_nll_jit(const HostPlan& plan, const ColPtrs& cols, long long n, const double* d_consts, int P,
+                             void* scratch, SumPair* d_out, unsigned long long* d_bad, cudaStream_t stream,
+                             cudaEvent_t ev_start = nullptr, cudaEvent_t ev_stop = nullptr);
+
+// Compiles the plan's kernels (the generated formulas + kernels_device.cuh, both kernel
+// instantiations) to sm_100a SASS without loading them: the CPU-side check of the
+// generated code (NVRTC needs no GPU).
+bool jit_compile_only(const HostPlan& plan, std::string* log);
+
+}  // namespace ffb

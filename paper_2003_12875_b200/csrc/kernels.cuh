@@ -12,16 +12,6 @@
 
 namespace ffb {
 
-struct ColPtrs {
-  const double* c[kMaxCols];
-};
-
-// Neumaier pair per parameter point (value = s + c).
-struct SumPair {
-  double s, c;
-};
-
-constexpr unsigned long long kNoInvalid = ~0ull;
 
 struct NllLaunchInfo {
   int threads = 0;
@@ -31,6 +21,7 @@ struct NllLaunchInfo {
   int nchunks = 0;
   int grid = 0;
   int launches = 0;
+  int jit = 0;  // 1: the formula-specialised (NVRTC) build ran
 };
 
 // Bytes of scratch the fused NLL launch needs for (n events, P points).
@@ -71,6 +62,12 @@ int launch_eval(const DevPlan& plan, const ColPtrs& cols, long long n, const dou
 // Combine R per-rank Neumaier pairs per point in fixed rank order (multi-GPU
 // exchange step after an all-gather): in = R x P pairs, out = P pairs.
 int launch_combine_ranks(const SumPair* d_in, int R, int P, SumPair* d_out, cudaStream_t stream);
+
+// Fixed-order fold of `ntiles` partial pairs per row into one pair per row.
+int launch_reduce(const SumPair* partial, int ntiles, int rows, SumPair* out, cudaStream_t stream);
+
+// Streaming multiprocessors of the current device (cached).
+int device_sm_count();
 
 // Test hook: which = 0 -> the kernel's exp, 1 -> its log, over n device doubles.
 int launch_math_probe(int which, const double* d_in, double* d_out, long long n, cudaStream_t stream);

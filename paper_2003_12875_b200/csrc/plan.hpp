@@ -13,7 +13,9 @@
 // This header is shared by the host compiler and nvcc.
 #pragma once
 
+#ifndef __CUDACC_RTC__
 #include <cstdint>
+#endif
 
 namespace ffb {
 
@@ -83,6 +85,17 @@ struct DevTerm {
   int flags;  // TermFlags
   int coff;   // offset of this term's constants in a point's constant row
 };
+
+struct ColPtrs {
+  const double* c[kMaxCols];
+};
+
+// Neumaier pair per parameter point (value = s + c).
+struct SumPair {
+  double s, c;
+};
+
+constexpr unsigned long long kNoInvalid = ~0ull;
 
 struct DevPlan {
   int nterms;

@@ -538,3 +538,25 @@ def read_soa_host(path: str) -> dict:
     cp = (DP * len(cols))(*[_dp(c) if c.size else _dp(np.empty(1)) for c in cols])
     _check(lib().ffcu_soa_read_host(str(path).encode(), cp))
     return dict(zip(names, cols))
+
+
+def expression_jit(enable=None) -> bool:
+    """Formula-specialised (NVRTC) builds for Expression pdfs: query (None) or set; returns
+    the previous setting."""
+    return bool(lib().ffcu_expression_jit(-1 if enable is None else (1 if enable else 0)))
+
+
+def expression_jit_status() -> str:
+    return lib().ffcu_expression_jit_status().decode()
+
+
+def expression_jit_source(model: Model, compile: bool = False) -> str:
+    """The generated straight-line formula code of a model (compile=True also NVRTC-compiles
+    the kernels around it; host only)."""
+    buf = ctypes.create_string_buffer(1 << 20)
+    _check(lib().ffcu_expression_jit_source(model.handle, 1 if compile else 0, buf, 1 << 20))
+    return buf.value.decode()
+
+
+def last_launch_jit(model: Model) -> bool:
+    return bool(lib().ffcu_last_launch_jit(model.handle))

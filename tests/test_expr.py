@@ -94,3 +94,21 @@ def test_expression_has_no_analytic_gradient():
     with pytest.raises(fb.FfitError) as e:
         fb.grad_slot_count(m)
     assert "Expression" in str(e.value)
+
+
+def test_formula_specialised_source_compiles_with_nvrtc():
+    """The generated straight-line formula code plus the fused kernels around it compile to
+    sm_100a SASS with NVRTC (host-side: no GPU needed) for the reference's Argus spelling."""
+    from paper_2003_12875_b200 import configs
+    m = fb.Model.from_string(configs.REFERENCE_TEXTS[configs.C2.name])
+    src = fb.expression_jit_source(m, compile=True)
+    assert "ffb_expr_batch" in src and "__ddiv_rn" in src and "__dsqrt_rn" in src
+    # constants travel bit-exactly (hex bit patterns, not decimal text)
+    assert "__longlong_as_double(0x3ff0000000000000ll)" in src
+
+
+def test_formula_source_mirrors_the_program():
+    m = fb.Model.from_string("observable x 0 2\nparameter a 0.5 0 1\n"
+                             "pdf e Expression(\"1 + a*x^3 - x^2/4 + pow(x, 2.5)\", x, a)\n")
+    src = fb.expression_jit_source(m)
+    assert src.count("__dmul_rn") >= 4 and "ffb_pow" in src and "k[2]" in src

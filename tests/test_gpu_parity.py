@@ -535,3 +535,33 @@ def test_expression_fit_uses_finite_differences():
     cols, _ = fb.sample_host(m, 20_000, 3)
     r = fb.fit_gradient(m, fb.DataSet.from_columns(cols), tolerance=1e-10, max_iterations=200)
     assert r.converged and not r.analytic_gradient
+
+
+@pytest.mark.parametrize("name", list(EXPR_MODELS) + ["c2_reference_text"])
+def test_expression_jit_matches_interpreter(name):
+    """The formula-specialised (NVRTC) build against the device interpreter: same formulas,
+    same operation order, same libdevice math -> the same values; both kernels (1 point:
+    streaming; 10 points: tile)."""
+    if name == "c2_reference_text":
+        text, col = configs.REFERENCE_TEXTS[configs.C2.name], "x"
+        cols, _ = fb.sample_host(fb.Model.from_string(configs.C2.text), 50_000, 9)
+        x = cols["x"]
+    else:
+        text, _, _, col = EXPR_MODELS[name]
+        x = np.load(os.path.join(GOLD, "expr_models.npz"))[f"{name}/x"]
+    m = fb.Model.from_string(text)
+    ds = fb.DataSet.from_columns({col: x})
+    pts = np.repeat(m.theta()[None, :], 10, axis=0)
+    was = fb.expression_jit(True)
+    try:
+        one_j, _, _ = fb.nll_points(m, ds, pts[:1])
+        assert fb.last_launch_jit(m), fb.expression_jit_status()
+        many_j, _, _ = fb.nll_points(m, ds, pts)
+        fb.expression_jit(False)
+        one_i, _, _ = fb.nll_points(m, ds, pts[:1])
+        assert not fb.last_launch_jit(m)
+        many_i, _, _ = fb.nll_points(m, ds, pts)
+    finally:
+        fb.expression_jit(was)
+    assert abs(one_j[0] - one_i[0]) <= 1e-15 * abs(one_i[0])
+    assert np.all(np.abs(many_j - many_i) <= 1e-15 * np.abs(many_i))
