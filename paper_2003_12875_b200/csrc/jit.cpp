@@ -214,14 +214,43 @@ std::string full_source(const HostPlan& plan) {
 
 std::string jit_expression_source(const HostPlan& plan) {
   std::ostringstream o;
+  // exp / log / sqrt take the kernels' table-driven, branch-free forms on their safe
+  // domains (<= 2 ulp, fastmath.cuh) and libdevice outside them, so NaN / inf / zero /
+  // negative arguments keep the IEEE results the reference would see
   o << "// generated by jit.cpp: the model's Expression formulas as straight-line device code\n"
        "#define FFB_EXPR_JIT 1\n"
+       "#include \"fastmath.cuh\"\n"
        "namespace ffb {\n"
        "__device__ __forceinline__ double ffb_pow(double a, double b) {\n"
        "  if (b == 2.0) return __dmul_rn(a, a);\n"
        "  if (b == 3.0) return __dmul_rn(__dmul_rn(a, a), a);\n"
        "  if (b == 4.0) { const double a2 = __dmul_rn(a, a); return __dmul_rn(a2, a2); }\n"
        "  return pow(a, b);\n"
+       "}\n"
+       // branch-free: the special cases are selected, not branched to, so the compiler
+       // keeps interleaving the E independent events of a thread
+       "__device__ __forceinline__ double ffb_exp(double a, const MathTables* __restrict__ tb) {\n"
+       "  const double r = fast_exp(a == a ? a : 0.0, tb);\n"
+       "  return a == a ? r : a;\n"
+       "}\n"
+       "__device__ __forceinline__ double ffb_log(double a, const MathTables* __restrict__ tb) {\n"
+       "  const double inf = __longlong_as_double(0x7ff0000000000000LL);\n"
+       "  const bool ok = a > 0.0 && a < inf;\n"
+       "  const double r = fast_log(ok ? a : 1.0, tb);\n"
+       "  return ok ? r : (a == 0.0 ? -inf : (a == inf ? inf : __longlong_as_double(0x7ff8000000000000LL)));\n"
+       "}\n"
+       "__device__ __forceinline__ double ffb_sqrt(double a) {\n"
+       "  const double inf = __longlong_as_double(0x7ff0000000000000LL);\n"
+       "  const bool ok = a > 0.0 && a < inf;\n"
+       "  const bool tiny = a < 0x1p-1000;\n"
+       "  double r = fast_sqrt_unit(ok ? (tiny ? a * 0x1p108 : a) : 1.0);\n"
+       "  r = tiny ? r * 0x1p-54 : r;\n"
+       "  return ok ? r : ((a == 0.0 || a == inf) ? a : __longlong_as_double(0x7ff8000000000000LL));\n"
+       "}\n"
+       // division by a point-uniform divisor: RN(1/d) hoisted by the compiler across the
+       // events, one correction step (div_by: the IEEE quotient bar rare 1-ulp cases)
+       "__device__ __forceinline__ double ffb_div_uniform(double a, double d) {\n"
+       "  return div_by(a, d, __drcp_rn(d));\n"
        "}\n";
   std::vector<int> offsets;
   for (int i = 0; i < plan.dev.nterms; ++i) {
@@ -234,17 +263,22 @@ std::string jit_expression_source(const HostPlan& plan) {
     // stack slots are named by depth: the postfix program is straight-line code
     int depth = 0, max_depth = 0;
     std::ostringstream body;
+    std::vector<bool> uni(kExprMaxDepth + 1, false);  // the slot depends on constants / parameters only
     for (std::size_t j = static_cast<std::size_t>(off); plan.programs[j].op != EX_END; ++j) {
       const ExprInstr& in = plan.programs[j];
       auto s = [](int d) { return "s" + std::to_string(d); };
       switch (in.op) {
-        case EX_CONST: body << "  " << s(depth) << " = " << hexbits(in.c) << ";\n"; ++depth; break;
-        case EX_VAR: body << "  " << s(depth) << " = k[" << 1 + in.slot << "];\n"; ++depth; break;
-        case EX_X: body << "  " << s(depth) << " = x;\n"; ++depth; break;
+        case EX_CONST: body << "  " << s(depth) << " = " << hexbits(in.c) << ";\n"; uni[depth] = true; ++depth; break;
+        case EX_VAR: body << "  " << s(depth) << " = k[" << 1 + in.slot << "];\n"; uni[depth] = true; ++depth; break;
+        case EX_X: body << "  " << s(depth) << " = x;\n"; uni[depth] = false; ++depth; break;
         case EX_ADD: --depth; body << "  " << s(depth - 1) << " = __dadd_rn(" << s(depth - 1) << ", " << s(depth) << ");\n"; break;
         case EX_SUB: --depth; body << "  " << s(depth - 1) << " = __dsub_rn(" << s(depth - 1) << ", " << s(depth) << ");\n"; break;
         case EX_MUL: --depth; body << "  " << s(depth - 1) << " = __dmul_rn(" << s(depth - 1) << ", " << s(depth) << ");\n"; break;
-        case EX_DIV: --depth; body << "  " << s(depth - 1) << " = __ddiv_rn(" << s(depth - 1) << ", " << s(depth) << ");\n"; break;
+        case EX_DIV:
+          --depth;
+          body << "  " << s(depth - 1) << " = " << (uni[depth] && !uni[depth - 1] ? "ffb_div_uniform(" : "__ddiv_rn(")
+               << s(depth - 1) << ", " << s(depth) << ");\n";
+          break;
         case EX_POW: --depth; body << "  " << s(depth - 1) << " = ffb_pow(" << s(depth - 1) << ", " << s(depth) << ");\n"; break;
         case EX_NEG: body << "  " << s(depth - 1) << " = -" << s(depth - 1) << ";\n"; break;
         case EX_SQUARE: body << "  " << s(depth - 1) << " = __dmul_rn(" << s(depth - 1) << ", " << s(depth - 1) << ");\n"; break;
@@ -257,27 +291,36 @@ std::string jit_expression_source(const HostPlan& plan) {
                << " = __dmul_rn(t, t); }\n";
           break;
         default: {
-          const char* f = in.op == EX_EXP ? "exp" : in.op == EX_LOG ? "log" : in.op == EX_SIN ? "sin"
-                        : in.op == EX_COS ? "cos" : in.op == EX_SQRT ? "__dsqrt_rn" : in.op == EX_ABS ? "fabs"
+          const bool tab = in.op == EX_EXP || in.op == EX_LOG;
+          const char* f = in.op == EX_EXP ? "ffb_exp" : in.op == EX_LOG ? "ffb_log" : in.op == EX_SIN ? "sin"
+                        : in.op == EX_COS ? "cos" : in.op == EX_SQRT ? "ffb_sqrt" : in.op == EX_ABS ? "fabs"
                         : in.op == EX_SINH ? "sinh" : "asinh";
-          body << "  " << s(depth - 1) << " = " << f << "(" << s(depth - 1) << ");\n";
+          body << "  " << s(depth - 1) << " = " << f << "(" << s(depth - 1) << (tab ? ", tb" : "") << ");\n";
           break;
         }
       }
+      switch (in.op) {  // binary operators: the result is uniform iff both operands were
+        case EX_ADD: case EX_SUB: case EX_MUL: case EX_DIV: case EX_POW:
+          uni[depth - 1] = uni[depth - 1] && uni[depth];
+          break;
+        default:
+          break;
+      }
       if (depth > max_depth) max_depth = depth;
     }
-    o << "__device__ __forceinline__ double ffb_expr_" << off << "(double x, const double* __restrict__ k) {\n";
-    o << "  (void)x; (void)k;\n";
+    o << "__device__ __forceinline__ double ffb_expr_" << off
+      << "(double x, const double* __restrict__ k, const MathTables* __restrict__ tb) {\n";
+    o << "  (void)x; (void)k; (void)tb;\n";
     for (int d = 0; d < max_depth; ++d) o << "  double s" << d << ";\n";
     o << body.str() << "  return s0;\n}\n";
   }
   o << "template <int E>\n"
        "__device__ __forceinline__ void ffb_expr_batch(int off, const double* __restrict__ k, const double (&x)[E],\n"
-       "                                               double (&v)[E]) {\n"
+       "                                               double (&v)[E], const MathTables* __restrict__ tb) {\n"
        "  switch (off) {\n";
   for (const int off : offsets) {
     o << "    case " << off << ":\n#pragma unroll\n      for (int e = 0; e < E; ++e) v[e] = ffb_expr_" << off
-      << "(x[e], k);\n      break;\n";
+      << "(x[e], k, tb);\n      break;\n";
   }
   o << "    default:\n      break;\n  }\n}\n}  // namespace ffb\n";
   return o.str();

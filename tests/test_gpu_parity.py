@@ -539,9 +539,10 @@ def test_expression_fit_uses_finite_differences():
 
 @pytest.mark.parametrize("name", list(EXPR_MODELS) + ["c2_reference_text"])
 def test_expression_jit_matches_interpreter(name):
-    """The formula-specialised (NVRTC) build against the device interpreter: same formulas,
-    same operation order, same libdevice math -> the same values; both kernels (1 point:
-    streaming; 10 points: tile)."""
+    """The formula-specialised (NVRTC) build against the device interpreter: same formulas in
+    the same operation order; exp / log / sqrt take the table-driven forms (<= 2 ulp) in the
+    specialised build, so the NLLs agree to 1e-13; both kernels (1 point: streaming; 10
+    points: tile)."""
     if name == "c2_reference_text":
         text, col = configs.REFERENCE_TEXTS[configs.C2.name], "x"
         cols, _ = fb.sample_host(fb.Model.from_string(configs.C2.text), 50_000, 9)
@@ -563,5 +564,5 @@ def test_expression_jit_matches_interpreter(name):
         many_i, _, _ = fb.nll_points(m, ds, pts)
     finally:
         fb.expression_jit(was)
-    assert abs(one_j[0] - one_i[0]) <= 1e-15 * abs(one_i[0])
-    assert np.all(np.abs(many_j - many_i) <= 1e-15 * np.abs(many_i))
+    assert abs(one_j[0] - one_i[0]) <= 1e-13 * abs(one_i[0])
+    assert np.all(np.abs(many_j - many_i) <= 1e-13 * np.abs(many_i))
