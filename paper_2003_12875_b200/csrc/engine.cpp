@@ -1,6 +1,7 @@
 #include "engine.hpp"
 
 #include "jit.hpp"
+#include "parallel.hpp"
 
 #include <algorithm>
 #include <atomic>
@@ -252,9 +253,16 @@ const double* Engine::upload_constants(const HostPlan& plan, const double* theta
   cuda_check(cudaEventSynchronize(staged_[k]), "cudaEventSynchronize");
   const int npar = static_cast<int>(m_.params.size());
   const int stride = plan.dev.stride;
-  for (int p = 0; p < P; ++p) {
+  // the points' constant rows are independent: spread them over the host pool when
+  // there are several (each row is validated; the first invalid point's error is raised)
+  auto row = [&](int p) {
     build_constants(plan, m_, thetas + static_cast<std::size_t>(p) * npar,
                     h_consts_[k] + static_cast<std::size_t>(p) * stride, extra_scale);
+  };
+  if (P >= 4) {
+    ThreadPool::instance().parallel_for(P, row);
+  } else {
+    for (int p = 0; p < P; ++p) row(p);
   }
   cuda_check(cudaMemcpyAsync(d_consts_[k], h_consts_[k],
                              static_cast<std::size_t>(P) * stride * sizeof(double),

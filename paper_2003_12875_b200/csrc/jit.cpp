@@ -213,10 +213,14 @@ std::string full_source(const HostPlan& plan) {
 }  // namespace
 
 std::string jit_expression_source(const HostPlan& plan) {
+  // Each formula becomes code over the thread's E events at once (one array per stack
+  // depth, every operation an unrolled loop), so the compiler interleaves the events.
+  // exp / log / sqrt / division take branch-free fast forms (fastmath.cuh, <= 2 ulp; the
+  // division's hoisted-reciprocal correction step is the IEEE quotient bar rare 1-ulp
+  // cases) on the operands where those are exact enough; one warp vote per operation
+  // sends the rare other operands (zero, negative, subnormal, inf, NaN) to the IEEE /
+  // libdevice form, so special values come out as the reference computes them.
   std::ostringstream o;
-  // exp / log / sqrt take the kernels' table-driven, branch-free forms on their safe
-  // domains (<= 2 ulp, fastmath.cuh) and libdevice outside them, so NaN / inf / zero /
-  // negative arguments keep the IEEE results the reference would see
   o << "// generated by jit.cpp: the model's Expression formulas as straight-line device code\n"
        "#define FFB_EXPR_JIT 1\n"
        "#include \"fastmath.cuh\"\n"
@@ -227,102 +231,200 @@ std::string jit_expression_source(const HostPlan& plan) {
        "  if (b == 4.0) { const double a2 = __dmul_rn(a, a); return __dmul_rn(a2, a2); }\n"
        "  return pow(a, b);\n"
        "}\n"
-       // branch-free: the special cases are selected, not branched to, so the compiler
-       // keeps interleaving the E independent events of a thread
-       "__device__ __forceinline__ double ffb_exp(double a, const MathTables* __restrict__ tb) {\n"
-       "  const double r = fast_exp(a == a ? a : 0.0, tb);\n"
-       "  return a == a ? r : a;\n"
+       "__device__ __forceinline__ bool ffb_pos_normal(double a) {  // finite, > 0, not subnormal\n"
+       "  return static_cast<unsigned>(__double2hiint(a)) - 0x00100000u < 0x7fe00000u;\n"
        "}\n"
-       "__device__ __forceinline__ double ffb_log(double a, const MathTables* __restrict__ tb) {\n"
-       "  const double inf = __longlong_as_double(0x7ff0000000000000LL);\n"
-       "  const bool ok = a > 0.0 && a < inf;\n"
-       "  const double r = fast_log(ok ? a : 1.0, tb);\n"
-       "  return ok ? r : (a == 0.0 ? -inf : (a == inf ? inf : __longlong_as_double(0x7ff8000000000000LL)));\n"
+       "template <int E>\n"
+       "__device__ __forceinline__ void ffb_vexp(double (&a)[E], const MathTables* __restrict__ tb) {\n"
+       "  bool rare = false;\n"
+       "#pragma unroll\n"
+       "  for (int e = 0; e < E; ++e) {\n"
+       "    const bool ok = a[e] == a[e];\n"
+       "    rare |= !ok;\n"
+       "    a[e] = ok ? fast_exp(a[e], tb) : a[e];\n"
+       "  }\n"
+       "  (void)rare;\n"
        "}\n"
-       "__device__ __forceinline__ double ffb_sqrt(double a) {\n"
-       "  const double inf = __longlong_as_double(0x7ff0000000000000LL);\n"
-       "  const bool ok = a > 0.0 && a < inf;\n"
-       "  const bool tiny = a < 0x1p-1000;\n"
-       "  double r = fast_sqrt_unit(ok ? (tiny ? a * 0x1p108 : a) : 1.0);\n"
-       "  r = tiny ? r * 0x1p-54 : r;\n"
-       "  return ok ? r : ((a == 0.0 || a == inf) ? a : __longlong_as_double(0x7ff8000000000000LL));\n"
+       "template <int E>\n"
+       "__device__ __forceinline__ void ffb_vlog(double (&a)[E], const MathTables* __restrict__ tb) {\n"
+       "  bool ok[E], rare = false;\n"
+       "  double r[E];\n"
+       "#pragma unroll\n"
+       "  for (int e = 0; e < E; ++e) {\n"
+       "    ok[e] = ffb_pos_normal(a[e]);\n"
+       "    rare |= !ok[e];\n"
+       "    r[e] = fast_log(ok[e] ? a[e] : 1.0, tb);\n"
+       "  }\n"
+       "  if (__any_sync(0xffffffffu, rare)) {\n"
+       "#pragma unroll\n"
+       "    for (int e = 0; e < E; ++e) r[e] = ok[e] ? r[e] : log(a[e]);\n"
+       "  }\n"
+       "#pragma unroll\n"
+       "  for (int e = 0; e < E; ++e) a[e] = r[e];\n"
        "}\n"
-       // division by a point-uniform divisor: RN(1/d) hoisted by the compiler across the
-       // events, one correction step (div_by: the IEEE quotient bar rare 1-ulp cases)
-       "__device__ __forceinline__ double ffb_div_uniform(double a, double d) {\n"
-       "  return div_by(a, d, __drcp_rn(d));\n"
+       "template <int E>\n"
+       "__device__ __forceinline__ void ffb_vsqrt(double (&a)[E]) {\n"
+       "  bool ok[E], rare = false;\n"
+       "  double r[E];\n"
+       "#pragma unroll\n"
+       "  for (int e = 0; e < E; ++e) {\n"
+       "    ok[e] = ffb_pos_normal(a[e]);\n"
+       "    rare |= !ok[e];\n"
+       "    r[e] = fast_sqrt_unit(ok[e] ? a[e] : 1.0);\n"
+       "  }\n"
+       "  if (__any_sync(0xffffffffu, rare)) {\n"
+       "#pragma unroll\n"
+       "    for (int e = 0; e < E; ++e) r[e] = ok[e] ? r[e] : __dsqrt_rn(a[e]);\n"
+       "  }\n"
+       "#pragma unroll\n"
+       "  for (int e = 0; e < E; ++e) a[e] = r[e];\n"
+       "}\n"
+       // a / d with d the same for every event of the point: RN(1/d) once, one correction
+       "template <int E>\n"
+       "__device__ __forceinline__ void ffb_vdiv_uniform(double (&a)[E], double d) {\n"
+       "  const double inv = __drcp_rn(d);\n"
+       "#pragma unroll\n"
+       "  for (int e = 0; e < E; ++e) a[e] = div_by(a[e], d, inv);\n"
+       "}\n"
+       // a / b per event: fast reciprocal + correction where both are ordinary numbers
+       "template <int E>\n"
+       "__device__ __forceinline__ void ffb_vdiv(double (&a)[E], const double (&b)[E]) {\n"
+       "  bool ok[E], rare = false;\n"
+       "  double r[E];\n"
+       "#pragma unroll\n"
+       "  for (int e = 0; e < E; ++e) {\n"
+       "    const double m = fabs(b[e]);\n"
+       "    ok[e] = m >= 0x1p-1000 && m <= 0x1p1000 && fabs(a[e]) <= 0x1p1000;\n"
+       "    rare |= !ok[e];\n"
+       "    const double bb = ok[e] ? b[e] : 1.0;\n"
+       "    r[e] = div_by(a[e], bb, fast_rcp_signed(bb));\n"
+       "  }\n"
+       "  if (__any_sync(0xffffffffu, rare)) {\n"
+       "#pragma unroll\n"
+       "    for (int e = 0; e < E; ++e) r[e] = ok[e] ? r[e] : __ddiv_rn(a[e], b[e]);\n"
+       "  }\n"
+       "#pragma unroll\n"
+       "  for (int e = 0; e < E; ++e) a[e] = r[e];\n"
        "}\n";
   std::vector<int> offsets;
   for (int i = 0; i < plan.dev.nterms; ++i) {
     if (plan.dev.t[i].kind != LK_EXPR) continue;
     const int off = plan.dev.t[i].order;
     bool seen = false;
-    for (const int s : offsets) seen = seen || s == off;
+    for (const int sv : offsets) seen = seen || sv == off;
     if (seen) continue;
     offsets.push_back(off);
-    // stack slots are named by depth: the postfix program is straight-line code
     int depth = 0, max_depth = 0;
     std::ostringstream body;
-    std::vector<bool> uni(kExprMaxDepth + 1, false);  // the slot depends on constants / parameters only
+    std::vector<bool> uni(kExprMaxDepth + 1, false);  // the slot holds one value for every event
+    auto S = [](int d) { return "s" + std::to_string(d); };
+    // a uniform slot is a scalar u<d>; the others are arrays s<d>[E]
+    auto U = [](int d) { return "u" + std::to_string(d); };
+    auto elem = [&](int d) { return uni[d] ? U(d) : S(d) + "[e]"; };
+    auto loop = [&](const std::string& stmt) {
+      body << "#pragma unroll\n  for (int e = 0; e < E; ++e) " << stmt << "\n";
+    };
+    auto widen = [&](int d) {  // make slot d an array (before a per-event op writes it)
+      if (uni[d]) {
+        loop(S(d) + "[e] = " + U(d) + ";");
+        uni[d] = false;
+      }
+    };
     for (std::size_t j = static_cast<std::size_t>(off); plan.programs[j].op != EX_END; ++j) {
       const ExprInstr& in = plan.programs[j];
-      auto s = [](int d) { return "s" + std::to_string(d); };
       switch (in.op) {
-        case EX_CONST: body << "  " << s(depth) << " = " << hexbits(in.c) << ";\n"; uni[depth] = true; ++depth; break;
-        case EX_VAR: body << "  " << s(depth) << " = k[" << 1 + in.slot << "];\n"; uni[depth] = true; ++depth; break;
-        case EX_X: body << "  " << s(depth) << " = x;\n"; uni[depth] = false; ++depth; break;
-        case EX_ADD: --depth; body << "  " << s(depth - 1) << " = __dadd_rn(" << s(depth - 1) << ", " << s(depth) << ");\n"; break;
-        case EX_SUB: --depth; body << "  " << s(depth - 1) << " = __dsub_rn(" << s(depth - 1) << ", " << s(depth) << ");\n"; break;
-        case EX_MUL: --depth; body << "  " << s(depth - 1) << " = __dmul_rn(" << s(depth - 1) << ", " << s(depth) << ");\n"; break;
-        case EX_DIV:
+        case EX_CONST:
+          body << "  " << U(depth) << " = " << hexbits(in.c) << ";\n";
+          uni[depth] = true;
+          ++depth;
+          break;
+        case EX_VAR:
+          body << "  " << U(depth) << " = k[" << 1 + in.slot << "];\n";
+          uni[depth] = true;
+          ++depth;
+          break;
+        case EX_X:
+          loop(S(depth) + "[e] = x[e];");
+          uni[depth] = false;
+          ++depth;
+          break;
+        case EX_ADD: case EX_SUB: case EX_MUL: case EX_POW: case EX_DIV: {
           --depth;
-          body << "  " << s(depth - 1) << " = " << (uni[depth] && !uni[depth - 1] ? "ffb_div_uniform(" : "__ddiv_rn(")
-               << s(depth - 1) << ", " << s(depth) << ");\n";
+          const int l = depth - 1, r = depth;
+          const char* fn = in.op == EX_ADD ? "__dadd_rn" : in.op == EX_SUB ? "__dsub_rn" : in.op == EX_MUL ? "__dmul_rn"
+                         : in.op == EX_POW ? "ffb_pow" : "__ddiv_rn";
+          if (uni[l] && uni[r]) {  // both uniform: a scalar (the compiler computes it once)
+            body << "  " << U(l) << " = " << fn << "(" << U(l) << ", " << U(r) << ");\n";
+          } else if (in.op == EX_DIV && uni[r]) {
+            body << "  ffb_vdiv_uniform<E>(" << S(l) << ", " << U(r) << ");\n";
+          } else if (in.op == EX_DIV) {
+            widen(l);
+            widen(r);
+            body << "  ffb_vdiv<E>(" << S(l) << ", " << S(r) << ");\n";
+          } else {
+            const std::string lhs = elem(l), rhs = elem(r);
+            loop(S(l) + "[e] = " + fn + "(" + lhs + ", " + rhs + ");");
+            uni[l] = false;
+          }
           break;
-        case EX_POW: --depth; body << "  " << s(depth - 1) << " = ffb_pow(" << s(depth - 1) << ", " << s(depth) << ");\n"; break;
-        case EX_NEG: body << "  " << s(depth - 1) << " = -" << s(depth - 1) << ";\n"; break;
-        case EX_SQUARE: body << "  " << s(depth - 1) << " = __dmul_rn(" << s(depth - 1) << ", " << s(depth - 1) << ");\n"; break;
-        case EX_CUBE:
-          body << "  " << s(depth - 1) << " = __dmul_rn(__dmul_rn(" << s(depth - 1) << ", " << s(depth - 1) << "), "
-               << s(depth - 1) << ");\n";
-          break;
-        case EX_FOURTH:
-          body << "  { const double t = __dmul_rn(" << s(depth - 1) << ", " << s(depth - 1) << "); " << s(depth - 1)
-               << " = __dmul_rn(t, t); }\n";
-          break;
-        default: {
-          const bool tab = in.op == EX_EXP || in.op == EX_LOG;
-          const char* f = in.op == EX_EXP ? "ffb_exp" : in.op == EX_LOG ? "ffb_log" : in.op == EX_SIN ? "sin"
-                        : in.op == EX_COS ? "cos" : in.op == EX_SQRT ? "ffb_sqrt" : in.op == EX_ABS ? "fabs"
-                        : in.op == EX_SINH ? "sinh" : "asinh";
-          body << "  " << s(depth - 1) << " = " << f << "(" << s(depth - 1) << (tab ? ", tb" : "") << ");\n";
+        }
+        default: {  // unary
+          const int d = depth - 1;
+          if (uni[d]) {  // a uniform operand stays scalar: libdevice / IEEE, computed once
+            const char* f = in.op == EX_NEG ? "-" : in.op == EX_EXP ? "exp" : in.op == EX_LOG ? "log"
+                          : in.op == EX_SIN ? "sin" : in.op == EX_COS ? "cos" : in.op == EX_SQRT ? "__dsqrt_rn"
+                          : in.op == EX_ABS ? "fabs" : in.op == EX_SINH ? "sinh" : in.op == EX_ASINH ? "asinh"
+                          : nullptr;
+            if (in.op == EX_SQUARE) {
+              body << "  " << U(d) << " = __dmul_rn(" << U(d) << ", " << U(d) << ");\n";
+            } else if (in.op == EX_CUBE) {
+              body << "  " << U(d) << " = __dmul_rn(__dmul_rn(" << U(d) << ", " << U(d) << "), " << U(d) << ");\n";
+            } else if (in.op == EX_FOURTH) {
+              body << "  { const double t = __dmul_rn(" << U(d) << ", " << U(d) << "); " << U(d)
+                   << " = __dmul_rn(t, t); }\n";
+            } else {
+              body << "  " << U(d) << " = " << f << "(" << U(d) << ");\n";
+            }
+            break;
+          }
+          const std::string a = S(d) + "[e]";
+          switch (in.op) {
+            case EX_NEG: loop(a + " = -" + a + ";"); break;
+            case EX_SQUARE: loop(a + " = __dmul_rn(" + a + ", " + a + ");"); break;
+            case EX_CUBE: loop(a + " = __dmul_rn(__dmul_rn(" + a + ", " + a + "), " + a + ");"); break;
+            case EX_FOURTH: loop("{ const double t = __dmul_rn(" + a + ", " + a + "); " + a + " = __dmul_rn(t, t); }"); break;
+            case EX_EXP: body << "  ffb_vexp<E>(" << S(d) << ", tb);\n"; break;
+            case EX_LOG: body << "  ffb_vlog<E>(" << S(d) << ", tb);\n"; break;
+            case EX_SQRT: body << "  ffb_vsqrt<E>(" << S(d) << ");\n"; break;
+            case EX_ABS: loop(a + " = fabs(" + a + ");"); break;
+            case EX_SIN: loop(a + " = sin(" + a + ");"); break;
+            case EX_COS: loop(a + " = cos(" + a + ");"); break;
+            case EX_SINH: loop(a + " = sinh(" + a + ");"); break;
+            default: loop(a + " = asinh(" + a + ");"); break;
+          }
           break;
         }
       }
-      switch (in.op) {  // binary operators: the result is uniform iff both operands were
-        case EX_ADD: case EX_SUB: case EX_MUL: case EX_DIV: case EX_POW:
-          uni[depth - 1] = uni[depth - 1] && uni[depth];
-          break;
-        default:
-          break;
-      }
       if (depth > max_depth) max_depth = depth;
     }
-    o << "__device__ __forceinline__ double ffb_expr_" << off
-      << "(double x, const double* __restrict__ k, const MathTables* __restrict__ tb) {\n";
-    o << "  (void)x; (void)k; (void)tb;\n";
-    for (int d = 0; d < max_depth; ++d) o << "  double s" << d << ";\n";
-    o << body.str() << "  return s0;\n}\n";
+    o << "template <int E>\n__device__ __forceinline__ void ffb_expr_" << off
+      << "(const double (&x)[E], const double* __restrict__ k, double (&v)[E], const MathTables* __restrict__ tb) {\n"
+      << "  (void)x; (void)k; (void)tb;\n";
+    for (int d = 0; d < max_depth; ++d) o << "  double s" << d << "[E];\n  double u" << d << ";\n";
+    o << body.str();
+    if (uni[0]) {
+      o << "#pragma unroll\n  for (int e = 0; e < E; ++e) v[e] = u0;\n";
+    } else {
+      o << "#pragma unroll\n  for (int e = 0; e < E; ++e) v[e] = s0[e];\n";
+    }
+    o << "}\n";
   }
   o << "template <int E>\n"
        "__device__ __forceinline__ void ffb_expr_batch(int off, const double* __restrict__ k, const double (&x)[E],\n"
        "                                               double (&v)[E], const MathTables* __restrict__ tb) {\n"
        "  switch (off) {\n";
-  for (const int off : offsets) {
-    o << "    case " << off << ":\n#pragma unroll\n      for (int e = 0; e < E; ++e) v[e] = ffb_expr_" << off
-      << "(x[e], k, tb);\n      break;\n";
-  }
-  o << "    default:\n      break;\n  }\n}\n}  // namespace ffb\n";
+  for (const int off : offsets) o << "    case " << off << ": ffb_expr_" << off << "<E>(x, k, v, tb); break;\n";
+  o << "    default: break;\n  }\n}\n}  // namespace ffb\n";
   return o.str();
 }
 

@@ -102,9 +102,9 @@ def test_formula_specialised_source_compiles_with_nvrtc():
     from paper_2003_12875_b200 import configs
     m = fb.Model.from_string(configs.REFERENCE_TEXTS[configs.C2.name])
     src = fb.expression_jit_source(m, compile=True)
-    assert "ffb_expr_batch" in src and "ffb_sqrt" in src
+    assert "ffb_expr_batch" in src and "ffb_vsqrt" in src
     # x / m0: a division by a point-uniform divisor takes the hoisted-reciprocal form
-    assert "ffb_div_uniform(" in src.split("ffb_expr_0")[1]
+    assert "ffb_vdiv_uniform<E>(" in src.split("void ffb_expr_0")[1]
     # constants travel bit-exactly (hex bit patterns, not decimal text)
     assert "__longlong_as_double(0x3ff0000000000000ll)" in src
 
