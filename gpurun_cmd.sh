@@ -1,3 +1,4 @@
-python bench.py --workload c2 --spelling reference --no-cpu-baseline --steps 3 --warmup 3 > gpurun_out/pre.json 2>gpurun_out/pre.err && \
-ncu --set full --clock-control none --import-source on -k regex:nll_kernel -s 5 -c 1 -o gpurun_out/prof_jit2 python bench.py --workload c2 --spelling reference --no-cpu-baseline --steps 3 --warmup 3 > gpurun_out/ncu_full.log 2>&1
-echo rc=$?
+for w in c1 c2 c4; do for wv in 8 2 4 16; do
+  FFB_NLL_WAVES=$wv python bench.py --workload $w --no-cpu-baseline --steps 20 > gpurun_out/ab.json 2>/dev/null
+  python -c "import json;d=json.load(open('gpurun_out/ab.json'));print('$w waves=$wv', '%.4e'%d['value'], d['config']['launch']['grid'])"
+done; done
