@@ -216,6 +216,12 @@ const char* ffcu_expression_jit_status(void);
 int ffcu_expression_jit_source(const ffit_model* m, int compile, char* buf, int cap);
 /* 1 if the model's last likelihood launch ran the formula-specialised build. */
 int ffcu_last_launch_jit(const ffit_model* m);
+/* The plan-specialised gradient pass (one point per launch: a fit's iteration) for
+ * single-column single-sum models: the generated term list / slot layout (compile_ks >=
+ * 0: also NVRTC-compile the kernel for that leaf-kind set, no GPU needed), and whether
+ * the model's last gradient launch ran it. */
+int ffcu_grad_spec_source(ffit_model* m, int compile_ks, char* buf, int cap);
+int ffcu_last_grad_jit(ffit_model* m);
 int ffcu_model_pdf_count(const ffit_model* m);
 const char* ffcu_model_pdf_name(const ffit_model* m, int i);
 int ffcu_model_observable_count(const ffit_model* m);

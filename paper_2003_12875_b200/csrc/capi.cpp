@@ -642,6 +642,29 @@ FFB_API int ffcu_expression_jit_source(const ffit_model* m, int compile, char* b
 
 FFB_API int ffcu_last_launch_jit(const ffit_model* m) { return m && m->engine->last_launch().jit ? 1 : 0; }
 
+FFB_API int ffcu_grad_spec_source(ffit_model* m, int compile_ks, char* buf, int cap) {
+  return guarded([&] {
+    require(m, "model");
+    const ffb::GradPlan& gp = engine(m).grad_plan();
+    if (!gp.ok) ffb::usage_error("analytic gradient unavailable for this model: " + gp.why);
+    const ffb::HostPlan& plan = m->engine->likelihood_plan();
+    if (compile_ks >= 0) {
+      std::string log;
+      if (!ffb::grad_spec_compile_only(plan, gp, compile_ks, &log)) {
+        ffb::numeric_error("NVRTC compile of the plan-specialised gradient pass failed: " + log.substr(0, 4000));
+      }
+    }
+    const std::string text = ffb::grad_spec_text(plan, gp);
+    if (buf && cap > 0) {
+      const std::size_t k = std::min<std::size_t>(text.size(), static_cast<std::size_t>(cap - 1));
+      std::memcpy(buf, text.data(), k);
+      buf[k] = '\0';
+    }
+  });
+}
+
+FFB_API int ffcu_last_grad_jit(ffit_model* m) { return m && engine(m).last_grad_jit() ? 1 : 0; }
+
 FFB_API int ffcu_model_pdf_count(const ffit_model* m) { return static_cast<int>(m->m->pdfs.size()); }
 
 FFB_API const char* ffcu_model_pdf_name(const ffit_model* m, int i) {

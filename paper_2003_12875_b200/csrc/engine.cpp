@@ -453,8 +453,13 @@ NllGradResult Engine::nll_grad_points(const DeviceDataset& ds, const double* the
           g_timer_events.emplace_back(ea, eb);
         }
       }
-      const NllLaunchInfo li = launch_nll_grad(plan_.dev, gp.dev, cols, ds.n, d_consts, np, d_scratch_, d_gslots_,
-                                               d_bad_, stream_, ks, ea, eb);
+      const bool spec = grad_spec_applies(plan_, gp, cols, np) && grad_spec_prepare(plan_, gp, ks);
+      const NllLaunchInfo li =
+          spec ? launch_nll_grad_spec(plan_, gp, cols, ds.n, d_consts, d_scratch_, d_gslots_, d_bad_, stream_, ks, ea,
+                                      eb)
+               : launch_nll_grad(plan_.dev, gp.dev, cols, ds.n, d_consts, np, d_scratch_, d_gslots_, d_bad_, stream_,
+                                 ks, ea, eb);
+      last_grad_jit_ = li.jit;
       cuda_check(cudaGetLastError(), "launch_nll_grad");
       r.launches += li.launches;
       count_launches(li.launches);

@@ -104,6 +104,7 @@ class Engine {
 
   // Current gradient layout (recompiled when parameters change constness).
   const GradPlan& grad_plan();
+  bool last_grad_jit() const { return last_grad_jit_ != 0; }
 
   // probabilities() (proj/src/eval.cpp:174-192): normalised per-event values.
   void probabilities(const DeviceDataset& ds, const double* theta, double* out, bool out_on_device,
@@ -145,6 +146,7 @@ class Engine {
   GradPlan grad_{};
   std::vector<bool> grad_const_;  // constness the layout was compiled for
   ExprInstr* d_prog_ = nullptr;  // device copy of plan_.programs
+  int last_grad_jit_ = 0;
   SumPair* d_gslots_ = nullptr;
   SumPair* h_gslots_ = nullptr;  // pinned
   std::size_t cap_gslots_ = 0;

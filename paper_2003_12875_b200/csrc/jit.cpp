@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <tuple>
 #include <memory>
 #include <mutex>
 #include <sstream>
@@ -426,6 +427,135 @@ std::string jit_expression_source(const HostPlan& plan) {
   for (const int off : offsets) o << "    case " << off << ": ffb_expr_" << off << "<E>(x, k, v, tb); break;\n";
   o << "    default: break;\n  }\n}\n}  // namespace ffb\n";
   return o.str();
+}
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// plan-specialised gradient pass (kernels_device.cuh nll_grad_spec_kernel)
+
+constexpr int kSpecE = 8;
+constexpr int kSpecTile = kJitThreads * kSpecE;
+
+struct SpecModule {
+  CUmodule mod = nullptr;
+  CUfunction fn = nullptr;
+  int occ = 1;
+};
+std::map<std::tuple<int, std::string, int>, SpecModule> g_spec;  // (device, source, kind set)
+
+std::string grad_spec_source(const HostPlan& plan, const GradPlan& gp) {
+  std::ostringstream o;
+  const int nt = plan.dev.nterms;
+  auto arr = [&](auto f) {
+    std::ostringstream a;
+    for (int i = 0; i < nt; ++i) a << (i ? ", " : "") << f(i);
+    return a.str();
+  };
+  o << "// generated by jit.cpp: the plan's term list and slot layout for nll_grad_spec_kernel\n"
+       "namespace ffb {\nstruct GradSpec {\n"
+    << "  static constexpr int nterms = " << nt << ";\n"
+    << "  static constexpr int kind[" << nt << "] = {" << arr([&](int i) { return plan.dev.t[i].kind; }) << "};\n"
+    << "  static constexpr int order[" << nt << "] = {" << arr([&](int i) { return plan.dev.t[i].order; }) << "};\n"
+    << "  static constexpr int pmask[" << nt << "] = {" << arr([&](int i) { return gp.dev.g[i].pmask; }) << "};\n"
+    << "  static constexpr int aslot[" << nt << "] = {" << arr([&](int i) { return gp.dev.g[i].slot; }) << "};\n"
+    << "  static constexpr int nslots = " << gp.dev.nslots << ";\n};\n}  // namespace ffb\n"
+    << "#define FFB_GRAD_SPEC 1\n#include \"kernels_device.cuh\"\n";
+  return o.str();
+}
+
+SpecModule* spec_module(const HostPlan& plan, const GradPlan& gp, int ks) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const std::string src = grad_spec_source(plan, gp);
+  const auto key = std::make_tuple(dev, src, ks);
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_spec.find(key);
+  if (it != g_spec.end()) return it->second.mod ? &it->second : nullptr;
+  SpecModule m;
+  DriverApi& drv = driver();
+  const std::string name = "&ffb::nll_grad_spec_kernel<" + std::to_string(kJitThreads) + ", " +
+                           std::to_string(kSpecE) + ", " + std::to_string(ks) + ">";
+  std::vector<char> cubin;
+  std::vector<std::string> lowered;
+  std::string log;
+  if (drv.ok && compile(src, {name}, &cubin, &lowered, &log)) {
+    cudaFree(nullptr);
+    if (drv.module_load(&m.mod, cubin.data()) == CUDA_SUCCESS &&
+        drv.get_function(&m.fn, m.mod, lowered[0].c_str()) == CUDA_SUCCESS) {
+      const int smem = kJitStages * kSpecTile * static_cast<int>(sizeof(double));
+      drv.set_attribute(m.fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem);
+      drv.occupancy(&m.occ, m.fn, kJitThreads, smem);
+      if (m.occ < 1) m.occ = 1;
+    } else {
+      m.mod = nullptr;
+    }
+  }
+  if (!m.mod) g_status = "gradient pass: generic kernels (" + (drv.ok ? log.substr(0, 2000) : drv.why) + ")";
+  auto& slot = g_spec[key];
+  slot = m;
+  return slot.mod ? &slot : nullptr;
+}
+
+}  // namespace
+
+std::string grad_spec_text(const HostPlan& plan, const GradPlan& gp) { return grad_spec_source(plan, gp); }
+
+bool grad_spec_compile_only(const HostPlan& plan, const GradPlan& gp, int ks, std::string* log) {
+  std::vector<char> cubin;
+  std::vector<std::string> low;
+  const std::string name = "&ffb::nll_grad_spec_kernel<" + std::to_string(kJitThreads) + ", " +
+                           std::to_string(kSpecE) + ", " + std::to_string(ks) + ">";
+  return compile(grad_spec_source(plan, gp), {name}, &cubin, &low, log);
+}
+
+bool grad_spec_applies(const HostPlan& plan, const GradPlan& gp, const ColPtrs& cols, int P) {
+  if (!jit_enabled() || !gp.ok || P != 1 || !plan.dev.simple || plan.dev.ncols != 1 || !plan.programs.empty()) {
+    return false;
+  }
+  if (std::getenv("FFB_NO_GRAD_SPEC") || std::getenv("FFB_NO_STREAM")) return false;
+  return (reinterpret_cast<uintptr_t>(cols.c[0]) & 15) == 0;
+}
+
+bool grad_spec_prepare(const HostPlan& plan, const GradPlan& gp, int ks) {
+  return spec_module(plan, gp, ks) != nullptr;
+}
+
+NllLaunchInfo launch_nll_grad_spec(const HostPlan& plan, const GradPlan& gp, const ColPtrs& cols, long long n,
+                                   const double* d_consts, void* scratch, SumPair* d_out,
+                                   unsigned long long* d_bad, cudaStream_t stream, int ks, cudaEvent_t ev_start,
+                                   cudaEvent_t ev_stop) {
+  NllLaunchInfo info;
+  SpecModule* m = spec_module(plan, gp, ks);
+  if (!m) usage_error("internal: launch_nll_grad_spec without a module");
+  DriverApi& drv = driver();
+  const long long ntl = (n + kSpecTile - 1) / kSpecTile;
+  long long G = static_cast<long long>(device_sm_count()) * m->occ;
+  if (G > ntl) G = ntl;
+  DevPlan dp = plan.dev;
+  ColPtrs cp = cols;
+  long long nn = n;
+  const double* kc = d_consts;
+  int ntiles = static_cast<int>(ntl);
+  SumPair* partial = static_cast<SumPair*>(scratch);
+  unsigned long long* bad = d_bad;
+  void* args[] = {&dp, &cp, &nn, &kc, &ntiles, &partial, &bad};
+  cudaMemsetAsync(d_bad, 0xff, sizeof(unsigned long long), stream);
+  if (ev_start) cudaEventRecord(ev_start, stream);
+  const CUresult rc = drv.launch(m->fn, static_cast<unsigned>(G), 1, 1, kJitThreads, 1, 1,
+                                 kJitStages * kSpecTile * sizeof(double), reinterpret_cast<CUstream>(stream), args,
+                                 nullptr);
+  if (ev_stop) cudaEventRecord(ev_stop, stream);
+  if (rc != CUDA_SUCCESS) numeric_error("cuLaunchKernel (plan-specialised gradient) failed: " + std::to_string(rc));
+  launch_reduce(partial, static_cast<int>(G), gp.dev.nslots, d_out, stream);
+  info.threads = kJitThreads;
+  info.events_per_thread = kSpecE;
+  info.tile = kSpecTile;
+  info.ntiles = static_cast<int>(ntl);
+  info.grid = static_cast<int>(G);
+  info.launches = 2;
+  info.jit = 1;
+  return info;
 }
 
 bool jit_enabled() { return g_enabled.load(); }

@@ -38,6 +38,17 @@ NllLaunchInfo launch_nll_jit(const HostPlan& plan, const ColPtrs& cols, long lon
                              void* scratch, SumPair* d_out, unsigned long long* d_bad, cudaStream_t stream,
                              cudaEvent_t ev_start = nullptr, cudaEvent_t ev_stop = nullptr);
 
+// Plan-specialised gradient pass (kernels_device.cuh nll_grad_spec_kernel): one point,
+// single-column single-sum plans without Expression leaves, aligned column.
+bool grad_spec_applies(const HostPlan& plan, const GradPlan& gp, const ColPtrs& cols, int P);
+bool grad_spec_prepare(const HostPlan& plan, const GradPlan& gp, int ks);  // compile / cache
+std::string grad_spec_text(const HostPlan& plan, const GradPlan& gp);
+bool grad_spec_compile_only(const HostPlan& plan, const GradPlan& gp, int ks, std::string* log);
+NllLaunchInfo launch_nll_grad_spec(const HostPlan& plan, const GradPlan& gp, const ColPtrs& cols, long long n,
+                                   const double* d_consts, void* scratch, SumPair* d_out,
+                                   unsigned long long* d_bad, cudaStream_t stream, int ks,
+                                   cudaEvent_t ev_start = nullptr, cudaEvent_t ev_stop = nullptr);
+
 // Compiles the plan's kernels (the generated formulas + kernels_device.cuh, both kernel
 // instantiations) to sm_100a SASS without loading them: the CPU-side check of the
 // generated code (NVRTC needs no GPU).

@@ -560,3 +560,15 @@ def expression_jit_source(model: Model, compile: bool = False) -> str:
 
 def last_launch_jit(model: Model) -> bool:
     return bool(lib().ffcu_last_launch_jit(model.handle))
+
+
+def grad_spec_source(model: Model, compile_ks=None) -> str:
+    """The plan-specialised gradient pass's generated spec (compile_ks = 0/1/2: also
+    NVRTC-compile the kernel for that leaf-kind set; host only)."""
+    buf = ctypes.create_string_buffer(1 << 16)
+    _check(lib().ffcu_grad_spec_source(model.handle, -1 if compile_ks is None else int(compile_ks), buf, 1 << 16))
+    return buf.value.decode()
+
+
+def last_grad_jit(model: Model) -> bool:
+    return bool(lib().ffcu_last_grad_jit(model.handle))
