@@ -245,6 +245,10 @@ int ffcu_result_trace(const ffit_fit_result* r, double* out, int cap);
 
 /* Last fused-NLL launch shape: threads, events/thread, tile, tiles, chunks, grid. */
 int ffcu_last_launch(const ffit_model* m, int* info6);
+/* Terms of the model's last likelihood launch served by the launch-constant branch cache
+ * (ArgusBG with m0 and p = 1/2 fixed over the launch's points: its data-only part computed
+ * once per staged tile; values bit-identical; FFB_NO_CONST_CACHE=1 turns it off). */
+int ffcu_last_launch_cached(const ffit_model* m);
 /* CUDA-event timing of every fused NLL kernel launch while enabled (on the
  * launching stream); _read synchronises, returns the summed ms and the launch
  * count, and clears. */

@@ -89,6 +89,7 @@ SIGNATURES = {
     "ffcu_expression_jit_status": (CP, []),
     "ffcu_expression_jit_source": (I, [VP, I, CP, I]),
     "ffcu_last_launch_jit": (I, [VP]),
+    "ffcu_last_launch_cached": (I, [VP]),
     "ffcu_grad_spec_source": (I, [VP, I, CP, I]),
     "ffcu_last_grad_jit": (I, [VP]),
     "ffcu_soa_write": (I, [CP, ctypes.POINTER(CP), ctypes.POINTER(DP), I, LL]),

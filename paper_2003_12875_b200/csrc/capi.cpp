@@ -935,6 +935,8 @@ FFB_API int ffcu_last_launch(const ffit_model* m, int* info6) {
   });
 }
 
+FFB_API int ffcu_last_launch_cached(const ffit_model* m) { return m ? m->engine->last_launch().cached : 0; }
+
 FFB_API unsigned long long ffcu_kernel_launches(void) { return ffb::kernel_launches(); }
 
 FFB_API int ffcu_kernel_timer(int enable) {

@@ -306,12 +306,16 @@ int Engine::nll_points_device(const DeviceDataset& ds, const double* thetas, int
         g_timer_events.emplace_back(ea, eb);
       }
     }
-    const int ks = plan_kind_set(plan_.dev, h_consts_[slot_], P);
     if (!plan_.programs.empty() && jit_prepare(plan_)) {
       // Expression leaves: the formula-specialised build (jit.cpp) instead of the interpreter
       last_ = launch_nll_jit(plan_, cols, ds.n, d_consts, P, d_scratch_, d_pairs, d_bad, s, ea, eb);
     } else {
-      last_ = launch_nll(plan_.dev, cols, ds.n, d_consts, P, d_scratch_, d_pairs, d_bad, s, ks, ea, eb);
+      // launch-constant branches (ArgusBG with m0 fixed over the launch) cached per tile
+      DevPlan lp = plan_.dev;
+      const int cached = cache_launch_constants(lp, h_consts_[slot_], P);
+      const int ks = plan_kind_set(lp, h_consts_[slot_], P);
+      last_ = launch_nll(lp, cols, ds.n, d_consts, P, d_scratch_, d_pairs, d_bad, s, ks, ea, eb);
+      last_.cached = cached;
     }
     launches = last_.launches;
     cuda_check(cudaGetLastError(), "launch_nll");

@@ -22,6 +22,7 @@ struct NllLaunchInfo {
   int grid = 0;
   int launches = 0;
   int jit = 0;  // 1: the formula-specialised (NVRTC) build ran
+  int cached = 0;  // terms served by the launch-constant branch cache
 };
 
 // Bytes of scratch the fused NLL launch needs for (n events, P points).
@@ -53,6 +54,13 @@ bool grad_layout_fits(const DevPlan& plan, const DevGradPlan& gp);
 // ArgusBG (p = 1/2, |c| <= 700), 1 = + Chebychev / Polynomial, 2 = everything
 // (ChiSquare, JohnsonSU, general ArgusBG).  host_consts: the P rows about to launch.
 int plan_kind_set(const DevPlan& plan, const double* host_consts, int P);
+
+// Launch-constant branch cache (plan.hpp DevDerive): rewrites, in `plan`, the ArgusBG
+// terms whose m0 and p = 1/2 are bitwise identical over the P rows about to launch
+// into LK_ARGUS_CACHED terms whose data-only part the tile kernel computes once per
+// tile.  Values are bit-identical to the uncached plan.  Returns the terms rewritten
+// (0 when P is small enough for the streaming build, or FFB_NO_CONST_CACHE is set).
+int cache_launch_constants(DevPlan& plan, const double* host_consts, int P);
 
 // Per-event values of the plan for one point (probabilities() when the plan is
 // normalised, PdfSpec::eval_batch when not).

@@ -38,6 +38,9 @@ enum LeafKind : int {
   LK_POLY = 6,     // c: [coef, a1..an]
   LK_EXPR = 7,     // c: [coef, v_0..v_{k-1}] (the formula's parameter values); order = program
                    // offset in DevPlan::prog
+  LK_ARGUS_CACHED = 8,  // c: as LK_ARGUS; order = shared-memory column of the tile's cached
+                        // (t, x sqrt t) pair (DevPlan::dv): ArgusBG with m0 and p = 1/2 the same
+                        // for every point of the launch (a launch-constant branch)
 };
 
 // Expression programs (expr.hpp): postfix instructions, END-terminated on the device.
@@ -97,6 +100,17 @@ struct SumPair {
 
 constexpr unsigned long long kNoInvalid = ~0ull;
 
+// Launch-constant branch cache (RooFit's constant-term optimisation, restated per
+// launch): an ArgusBG term whose m0 and p = 1/2 are identical for every point of the
+// launch has a data-only part t = 1 - (x/m0)^2, u = x sqrt(t) (both 0 for t <= 0) that
+// the tile kernel computes ONCE per staged tile into two extra shared-memory columns;
+// each point then evaluates u * exp(c t) (cache_launch_constants, kernels.cu).
+constexpr int kMaxDerived = 2;
+struct DevDerive {
+  int col;   // source data column
+  int coff;  // the term's offset in a point's constant row (m0 = [1], 1/m0 = [4])
+};
+
 struct DevPlan {
   int nterms;
   int ncols;   // distinct observables read
@@ -104,6 +118,8 @@ struct DevPlan {
   int simple;  // 1: a single sum of terms (no product structure)
   DevTerm t[kMaxTerms];
   const ExprInstr* prog;  // device copy of the plan's Expression programs (or null)
+  int nderived = 0;       // launch-constant caches (tile kernel only); 2 smem columns each
+  DevDerive dv[kMaxDerived] = {};
 };
 
 // Fused NLL + gradient pass (kernels.cu nll_grad_kernel).  With W_f(x) = the product

@@ -562,6 +562,11 @@ def last_launch_jit(model: Model) -> bool:
     return bool(lib().ffcu_last_launch_jit(model.handle))
 
 
+def last_launch_cached(model: Model) -> int:
+    """Terms of the last likelihood launch served by the launch-constant branch cache."""
+    return int(lib().ffcu_last_launch_cached(model.handle))
+
+
 def grad_spec_source(model: Model, compile_ks=None) -> str:
     """The plan-specialised gradient pass's generated spec (compile_ks = 0/1/2: also
     NVRTC-compile the kernel for that leaf-kind set; host only)."""

@@ -104,6 +104,61 @@ def test_points_are_independent_of_batching():
     assert np.array_equal(again, full)  # deterministic run to run
 
 
+def test_launch_constant_cache_is_bit_identical():
+    """ArgusBG with m0 (and p = 1/2) fixed over a launch's points is served by the
+    per-tile launch-constant cache; adding one point with another m0 turns the cache
+    off for that launch.  The shared points' values are bitwise equal either way, and
+    match the oracle."""
+    w = configs.C2
+    m, ds, cols, o = setup(w.text, 150_007, 21)
+    pts = w.points(m, n_points=16)
+    j = m.param_names.index("m0")
+    assert np.all(pts[:, j] == pts[0, j])
+    cached, bad, _ = fb.nll_points(m, ds, pts)
+    assert fb.last_launch_cached(m) == 1
+    other = pts[:1].copy()
+    other[0, j] = pts[0, j] * (1 + 1e-4)
+    plain, _, _ = fb.nll_points(m, ds, np.vstack([pts, other]))
+    assert fb.last_launch_cached(m) == 0
+    assert np.array_equal(cached, plain[:16])
+    for p in (0, 7, 15):
+        _, comp, ob = o.nll(cols, pts[p])
+        assert bad[p] == ob == -1
+        assert abs(cached[p] - comp) <= NLL_TOL * abs(comp)
+    # a ragged last tile, events at the range edge and at / beyond m0 (t <= 0: the
+    # Argus component is 0 there, the Gaussian keeps p > 0)
+    x = np.concatenate([cols[0][:5000], [pts[0, j], 5.2905, 5.29, 5.2]])
+    ds2 = fb.DataSet.from_columns({"x": x})
+    v2, b2, _ = fb.nll_points(m, ds2, pts)
+    assert fb.last_launch_cached(m) == 1
+    for p in (0, 9):
+        _, comp, ob = o.nll([x], pts[p])
+        assert b2[p] == ob == -1
+        assert abs(v2[p] - comp) <= NLL_TOL * abs(comp)
+    # an Argus-only model: t <= 0 gives p = 0, the first such event is reported
+    text = """
+observable x 5.2 5.29
+parameter m0 5.28 5.0 5.4 const
+parameter c -20 -100 0
+parameter p 0.5 0 3 const
+pdf bkg ArgusBG(x, m0, c, p)
+"""
+    ma, oa = fb.Model.from_string(text), OracleModel(text)
+    xa = np.random.default_rng(2).uniform(5.2, 5.279, 9000)
+    xa[7000] = 5.285
+    pa = np.array([[5.28, -20.0 * (1 + 0.01 * i), 0.5] for i in range(12)])
+    va, ba, _ = fb.nll_points(ma, fb.DataSet.from_columns({"x": xa}), pa)
+    assert fb.last_launch_cached(ma) == 1
+    for p in (0, 11):
+        _, comp, ob = oa.nll([xa], pa[p])
+        assert ba[p] == ob == 7000 and va[p] == comp == math.inf
+    xa[7000] = 5.25
+    va, ba, _ = fb.nll_points(ma, fb.DataSet.from_columns({"x": xa}), pa)
+    for p in (0, 11):
+        _, comp, ob = oa.nll([xa], pa[p])
+        assert ba[p] == ob == -1 and abs(va[p] - comp) <= NLL_TOL * abs(comp)
+
+
 def test_more_than_512_points_split_launches():
     w = configs.C1
     m, ds, cols, o = setup(w.text, 20_000, 3)
