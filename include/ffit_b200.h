@@ -214,8 +214,19 @@ const char* ffcu_expression_jit_status(void);
 /* The generated formula source of a model (compile = 1: also NVRTC-compile the kernels
  * around it, no GPU needed); at most cap-1 characters into buf. */
 int ffcu_expression_jit_source(const ffit_model* m, int compile, char* buf, int cap);
-/* 1 if the model's last likelihood launch ran the formula-specialised build. */
+/* The build the model's last likelihood launch ran: 0 the static kernels, 1 the
+ * formula-specialised build, 2 the plan-specialised build (below). */
 int ffcu_last_launch_jit(const ffit_model* m);
+/* Plan-specialised likelihood builds: launches of more than 8 points and at least
+ * FFB_PLAN_SPEC_MIN (default 5e7) event-points of models without Expression pdfs run the
+ * tile kernel compiled at run time (NVRTC) around the launch's term list; values as the
+ * static build's; FFB_NO_PLAN_SPEC=1 (or ffcu_expression_jit(0)) turns it off.  The
+ * generated source for P points (points may be null: the model's plan as is); compile = 1
+ * also NVRTC-compiles it (no GPU needed); at most cap-1 characters into buf. */
+int ffcu_plan_spec_source(ffit_model* m, const double* points, int P, int compile, char* buf, int cap);
+/* The event-point threshold of the plan-specialised builds: v >= 0 sets it, -1 turns the
+ * builds off, -2 only queries; returns the previous value (-1: off). */
+double ffcu_plan_spec_min_work(double v);
 /* The plan-specialised gradient pass (one point per launch: a fit's iteration) for
  * single-column single-sum models: the generated term list / slot layout (compile_ks >=
  * 0: also NVRTC-compile the kernel for that leaf-kind set, no GPU needed), and whether

@@ -640,7 +640,41 @@ FFB_API int ffcu_expression_jit_source(const ffit_model* m, int compile, char* b
   });
 }
 
-FFB_API int ffcu_last_launch_jit(const ffit_model* m) { return m && m->engine->last_launch().jit ? 1 : 0; }
+FFB_API int ffcu_last_launch_jit(const ffit_model* m) { return m && m->engine ? m->engine->last_launch().jit : 0; }
+
+FFB_API double ffcu_plan_spec_min_work(double v) { return ffb::plan_spec_min_work(v); }
+
+FFB_API int ffcu_plan_spec_source(ffit_model* m, const double* points, int P, int compile, char* buf, int cap) {
+  return guarded([&] {
+    require(m, "model");
+    const ffb::HostPlan& plan = engine(m).likelihood_plan();
+    if (!plan.programs.empty()) ffb::usage_error("models with Expression pdfs take the formula-specialised build");
+    ffb::DevPlan lp = plan.dev;
+    std::vector<double> rows;
+    if (points && P > 0) {  // the launch-constant rewrite these points would get
+      const std::size_t npar = m->m->params.size();
+      rows.resize(static_cast<std::size_t>(P) * plan.dev.stride);
+      for (int p = 0; p < P; ++p) {
+        ffb::build_constants(plan, *m->m, points + p * npar, rows.data() + static_cast<std::size_t>(p) * plan.dev.stride,
+                             std::ldexp(1.0, ffb::kPScaleLog2));
+      }
+      ffb::cache_launch_constants(lp, rows.data(), P);
+    }
+    const std::string text = ffb::plan_spec_source(lp);
+    if (compile) {
+      const int ks = rows.empty() ? 2 : ffb::plan_kind_set(lp, rows.data(), P);
+      std::string log;
+      if (!ffb::plan_spec_compile_only(lp, ks, &log)) {
+        ffb::numeric_error("NVRTC compile of the plan-specialised likelihood failed: " + log.substr(0, 4000));
+      }
+    }
+    if (buf && cap > 0) {
+      const std::size_t k = std::min<std::size_t>(text.size(), static_cast<std::size_t>(cap - 1));
+      std::memcpy(buf, text.data(), k);
+      buf[k] = '\0';
+    }
+  });
+}
 
 FFB_API int ffcu_grad_spec_source(ffit_model* m, int compile_ks, char* buf, int cap) {
   return guarded([&] {

@@ -314,7 +314,12 @@ int Engine::nll_points_device(const DeviceDataset& ds, const double* thetas, int
       DevPlan lp = plan_.dev;
       const int cached = cache_launch_constants(lp, h_consts_[slot_], P);
       const int ks = plan_kind_set(lp, h_consts_[slot_], P);
-      last_ = launch_nll(lp, cols, ds.n, d_consts, P, d_scratch_, d_pairs, d_bad, s, ks, ea, eb);
+      if (plan_spec_applies(plan_, lp, ds.n, P) && plan_spec_prepare(lp, ks)) {
+        // the tile kernel compiled around this launch's term list (jit.cpp; cached)
+        last_ = launch_nll_spec(lp, cols, ds.n, d_consts, P, d_scratch_, d_pairs, d_bad, s, ks, nll_waves(), ea, eb);
+      } else {
+        last_ = launch_nll(lp, cols, ds.n, d_consts, P, d_scratch_, d_pairs, d_bad, s, ks, ea, eb);
+      }
       last_.cached = cached;
     }
     launches = last_.launches;

@@ -191,6 +191,14 @@ bool compile(const std::string& source, const std::vector<std::string>& names, s
     api.cubin_size(prog, &cs);
     cubin->resize(cs);
     api.cubin(prog, cubin->data());
+    if (const char* dump = std::getenv("FFB_JIT_DUMP")) {  // debugging: cuobjdump the generated builds
+      static std::atomic<int> seq{0};
+      const std::string path = std::string(dump) + "." + std::to_string(seq++) + ".cubin";
+      if (FILE* f = std::fopen(path.c_str(), "wb")) {
+        std::fwrite(cubin->data(), 1, cs, f);
+        std::fclose(f);
+      }
+    }
     for (const auto& n : names) {
       const char* low = nullptr;
       if (api.lowered(prog, n.c_str(), &low) != NVRTC_SUCCESS || !low) {
@@ -687,6 +695,152 @@ NllLaunchInfo launch_nll_jit(const HostPlan& plan, const ColPtrs& cols, long lon
   info.ntiles = static_cast<int>(ntl);
   info.launches = 2;
   info.jit = 1;
+  return info;
+}
+
+// ---------------------------------------------------------------------------
+// plan-specialised likelihood (kernels_device.cuh eval_plan_spec): the launch's term
+// list (after the launch-constant rewrite) as compile-time constants of the tile kernel
+
+namespace {
+
+struct PlanModule {
+  CUmodule mod = nullptr;
+  CUfunction fn = nullptr;
+  int occ = 1;
+};
+std::map<std::tuple<int, std::string, int>, PlanModule> g_plan_mods;  // (device, source, mode)
+
+int spec_mode(const DevPlan& d, int ks) { return ks + (d.simple ? 0 : 3) + (d.nderived > 0 ? 6 : 0); }
+
+std::string plan_spec_kernel_name(const DevPlan& d, int ks) {
+  return "&ffb::nll_kernel<" + std::to_string(kJitThreads) + ", " + std::to_string(kJitE) + ", " +
+         (d.ncols == 1 ? "true" : "false") + ", 2, " + std::to_string(spec_mode(d, ks)) + ", ffb::PlanSpec>";
+}
+
+PlanModule* plan_module(const DevPlan& d, int ks) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const std::string src = plan_spec_source(d);
+  const auto key = std::make_tuple(dev, src, spec_mode(d, ks));
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_plan_mods.find(key);
+  if (it != g_plan_mods.end()) return it->second.mod ? &it->second : nullptr;
+  PlanModule m;  // failures are cached too: no recompile per launch
+  DriverApi& drv = driver();
+  const std::string name = plan_spec_kernel_name(d, ks);
+  std::vector<char> cubin;
+  std::vector<std::string> lowered;
+  std::string log;
+  if (drv.ok && compile(src, {name}, &cubin, &lowered, &log)) {
+    cudaFree(nullptr);
+    if (drv.module_load(&m.mod, cubin.data()) == CUDA_SUCCESS &&
+        drv.get_function(&m.fn, m.mod, lowered[0].c_str()) == CUDA_SUCCESS) {
+      drv.set_attribute(m.fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
+                        kMaxCols * kJitTile * static_cast<int>(sizeof(double)));
+      drv.occupancy(&m.occ, m.fn, kJitThreads, (d.ncols + 2 * d.nderived) * kJitTile * sizeof(double));
+      if (m.occ < 1) m.occ = 1;
+    } else {
+      m.mod = nullptr;
+    }
+  }
+  if (!m.mod) g_status = "likelihood: generic kernels (" + (drv.ok ? log.substr(0, 2000) : drv.why) + ")";
+  auto& slot = g_plan_mods[key];
+  slot = m;
+  return slot.mod ? &slot : nullptr;
+}
+
+}  // namespace
+
+std::string plan_spec_source(const DevPlan& d) {
+  std::ostringstream o;
+  o << "// generated by jit.cpp: the launch's term list for nll_kernel<..., PlanSpec>\n"
+       "#include \"plan.hpp\"\nnamespace ffb {\nstruct PlanSpec {\n"
+       "  static constexpr bool kOn = true;\n"
+    << "  static constexpr int nterms = " << d.nterms << ";\n"
+    << "  static constexpr bool simple = " << (d.simple ? "true" : "false") << ";\n"
+    << "  static constexpr DevTerm t[" << d.nterms << "] = {";
+  for (int i = 0; i < d.nterms; ++i) {
+    const DevTerm& t = d.t[i];
+    o << (i ? ", " : "") << "{" << t.kind << ", " << t.col << ", " << t.order << ", " << t.flags << ", " << t.coff
+      << "}";
+  }
+  o << "};\n};\n}  // namespace ffb\n#include \"kernels_device.cuh\"\n";
+  return o.str();
+}
+
+namespace {
+std::atomic<double> g_spec_min{[] {
+  if (std::getenv("FFB_NO_PLAN_SPEC")) return -1.0;
+  const char* v = std::getenv("FFB_PLAN_SPEC_MIN");
+  return v ? std::atof(v) : 5e7;
+}()};
+}  // namespace
+
+double plan_spec_min_work(double v) {
+  const double was = g_spec_min.load();
+  if (v >= 0.0 || v == -1.0) g_spec_min.store(v);
+  return was;
+}
+
+bool plan_spec_applies(const HostPlan& plan, const DevPlan& launch, long long n, int P) {
+  const double min_work = g_spec_min.load();
+  if (min_work < 0.0 || !jit_enabled() || !plan.programs.empty()) return false;
+  if (P <= kJitStreamMaxP || launch.nterms < 1) return false;  // the streaming build serves few points
+  return static_cast<double>(n) * P >= min_work;
+}
+
+bool plan_spec_prepare(const DevPlan& launch, int ks) { return plan_module(launch, ks) != nullptr; }
+
+bool plan_spec_compile_only(const DevPlan& launch, int ks, std::string* log) {
+  std::vector<char> cubin;
+  std::vector<std::string> low;
+  return compile(plan_spec_source(launch), {plan_spec_kernel_name(launch, ks)}, &cubin, &low, log);
+}
+
+NllLaunchInfo launch_nll_spec(const DevPlan& launch, const ColPtrs& cols, long long n, const double* d_consts, int P,
+                              void* scratch, SumPair* d_out, unsigned long long* d_bad, cudaStream_t stream, int ks,
+                              int waves, cudaEvent_t ev_start, cudaEvent_t ev_stop) {
+  NllLaunchInfo info;
+  if (P <= 0) return info;
+  PlanModule* m = plan_module(launch, ks);
+  if (!m) usage_error("internal: launch_nll_spec without a module");
+  DriverApi& drv = driver();
+  DevPlan dp = launch;
+  ColPtrs cp = cols;
+  long long nn = n;
+  const double* kc = d_consts;
+  int PP = P;
+  SumPair* partial = static_cast<SumPair*>(scratch);
+  unsigned long long* bad = d_bad;
+  cudaMemsetAsync(d_bad, 0xff, sizeof(unsigned long long) * P, stream);
+  long long ntl = (n + kJitTile - 1) / kJitTile;
+  if (ntl < 1) ntl = 1;
+  int ntiles = static_cast<int>(ntl);
+  // the static builds' grid rule (kernels.cu nll_shape): >= `waves` waves of resident CTAs
+  const long long slots = static_cast<long long>(device_sm_count()) * m->occ;
+  long long want = (waves * slots + ntiles - 1) / ntiles;
+  if (want < 1) want = 1;
+  if (want > P) want = P;
+  int pchunk = static_cast<int>((P + want - 1) / want);
+  const int nchunks = (P + pchunk - 1) / pchunk;
+  void* args[] = {&dp, &cp, &nn, &kc, &PP, &pchunk, &ntiles, &partial, &bad};
+  if (ev_start) cudaEventRecord(ev_start, stream);
+  const CUresult rc =
+      drv.launch(m->fn, static_cast<unsigned>(static_cast<long long>(ntiles) * nchunks), 1, 1, kJitThreads, 1, 1,
+                 (launch.ncols + 2 * launch.nderived) * kJitTile * sizeof(double),
+                 reinterpret_cast<CUstream>(stream), args, nullptr);
+  if (ev_stop) cudaEventRecord(ev_stop, stream);
+  if (rc != CUDA_SUCCESS) numeric_error("cuLaunchKernel (plan-specialised likelihood) failed: " + std::to_string(rc));
+  launch_reduce(partial, ntiles, P, d_out, stream);
+  info.threads = kJitThreads;
+  info.events_per_thread = kJitE;
+  info.tile = kJitTile;
+  info.ntiles = ntiles;
+  info.nchunks = nchunks;
+  info.grid = ntiles * nchunks;
+  info.launches = 2;
+  info.jit = 2;
   return info;
 }
 

@@ -49,6 +49,22 @@ NllLaunchInfo launch_nll_grad_spec(const HostPlan& plan, const GradPlan& gp, con
                                    unsigned long long* d_bad, cudaStream_t stream, int ks,
                                    cudaEvent_t ev_start = nullptr, cudaEvent_t ev_stop = nullptr);
 
+// Plan-specialised likelihood builds (kernels_device.cuh eval_plan_spec): the tile
+// kernel compiled at run time around the launch's term list (kinds, columns, flags,
+// constant offsets as compile-time constants; the launch-constant rewrite included), for
+// launches of more than kStreamMaxP points and at least FFB_PLAN_SPEC_MIN (default 5e7)
+// event-points; models without Expression leaves.  FFB_NO_PLAN_SPEC=1 turns it off.
+std::string plan_spec_source(const DevPlan& launch);
+// Sets the event-point threshold (v >= 0; -1 turns the builds off; other negatives only
+// query); returns the previous setting.
+double plan_spec_min_work(double v);
+bool plan_spec_applies(const HostPlan& plan, const DevPlan& launch, long long n, int P);
+bool plan_spec_prepare(const DevPlan& launch, int ks);  // compile / cache
+bool plan_spec_compile_only(const DevPlan& launch, int ks, std::string* log);
+NllLaunchInfo launch_nll_spec(const DevPlan& launch, const ColPtrs& cols, long long n, const double* d_consts, int P,
+                              void* scratch, SumPair* d_out, unsigned long long* d_bad, cudaStream_t stream, int ks,
+                              int waves, cudaEvent_t ev_start = nullptr, cudaEvent_t ev_stop = nullptr);
+
 // Compiles the plan's kernels (the generated formulas + kernels_device.cuh, both kernel
 // instantiations) to sm_100a SASS without loading them: the CPU-side check of the
 // generated code (NVRTC needs no GPU).

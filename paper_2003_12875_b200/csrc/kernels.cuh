@@ -74,6 +74,9 @@ int launch_combine_ranks(const SumPair* d_in, int R, int P, SumPair* d_out, cuda
 // Fixed-order fold of `ntiles` partial pairs per row into one pair per row.
 int launch_reduce(const SumPair* partial, int ntiles, int rows, SumPair* out, cudaStream_t stream);
 
+// Target waves of the tile kernel's (tile x point-chunk) grid (FFB_NLL_WAVES).
+int nll_waves();
+
 // Streaming multiprocessors of the current device (cached).
 int device_sm_count();
 

@@ -558,8 +558,27 @@ def expression_jit_source(model: Model, compile: bool = False) -> str:
     return buf.value.decode()
 
 
-def last_launch_jit(model: Model) -> bool:
-    return bool(lib().ffcu_last_launch_jit(model.handle))
+def last_launch_jit(model: Model) -> int:
+    """0: static kernels, 1: formula-specialised build, 2: plan-specialised build."""
+    return int(lib().ffcu_last_launch_jit(model.handle))
+
+
+def plan_spec_min_work(v: float = -2.0) -> float:
+    """Event-point threshold of the plan-specialised builds (-1: off); returns the old one."""
+    return float(lib().ffcu_plan_spec_min_work(float(v)))
+
+
+def plan_spec_source(model: Model, points=None, compile: bool = False) -> str:
+    """The plan-specialised likelihood source for a launch over `points` (compile: also
+    NVRTC-compile it; no GPU needed)."""
+    buf = ctypes.create_string_buffer(1 << 16)
+    if points is None:
+        _check(lib().ffcu_plan_spec_source(model.handle, None, 0, 1 if compile else 0, buf, len(buf)))
+    else:
+        pts = _f64(np.atleast_2d(points))
+        _check(lib().ffcu_plan_spec_source(model.handle, _dp(pts), pts.shape[0], 1 if compile else 0, buf,
+                                           len(buf)))
+    return buf.value.decode()
 
 
 def last_launch_cached(model: Model) -> int:

@@ -621,3 +621,41 @@ def test_expression_jit_matches_interpreter(name):
         fb.expression_jit(was)
     assert abs(one_j[0] - one_i[0]) <= 1e-13 * abs(one_i[0])
     assert np.all(np.abs(many_j - many_i) <= 1e-13 * np.abs(many_i))
+
+
+# ------------------------------------------------------------------ plan-specialised builds
+
+def _spec_cases():
+    from tests.test_gpu_grad import CASES
+    return CASES
+
+
+@pytest.mark.parametrize("name", list(_spec_cases()))
+def test_plan_specialised_build_matches_static_build(name):
+    """The tile kernel compiled around the launch's term list (jit.cpp plan_spec_source)
+    against the static build on the same launch, and against the oracle."""
+    from tests.test_gpu_grad import setup as grad_setup  # uniform events where no sampler exists
+    text, n = _spec_cases()[name]
+    m, ds, cols = grad_setup(text, n, 101)
+    o = OracleModel(text)
+    base = m.theta()
+    free = [k for k, nm in enumerate(m.param_names) if not m.is_constant(nm)]
+    pts = np.tile(base, (12, 1))
+    for p in range(12):
+        for k in free:
+            pts[p, k] = base[k] * (1.0 + 2e-4 * (p - 6)) if base[k] != 0 else 1e-4 * (p - 6)
+    old = fb.plan_spec_min_work(-1)
+    try:
+        static, sbad, _ = fb.nll_points(m, ds, pts)
+        assert fb.last_launch_jit(m) == 0
+        fb.plan_spec_min_work(0)
+        spec, bad, _ = fb.nll_points(m, ds, pts)
+        assert fb.last_launch_jit(m) == 2, fb.expression_jit_status()
+    finally:
+        fb.plan_spec_min_work(old)
+    assert np.array_equal(bad, sbad)
+    assert np.array_equal(spec, static), np.max(np.abs(spec - static) / np.abs(static))
+    for p in (0, 11):
+        _, comp, ob = o.nll(cols, pts[p])
+        assert bad[p] == ob
+        assert abs(spec[p] - comp) <= NLL_TOL * abs(comp)

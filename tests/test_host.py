@@ -273,3 +273,28 @@ def test_coefficient_derivatives(name):
             ests.append((8 * (C(h) - C(-h)) - (C(2 * h) - C(-2 * h))) / (12 * h))
         err = np.min(np.abs(np.array(ests) - d), axis=0)
         assert np.all(err <= 1e-9 * np.maximum(np.abs(d), base)), (pn, err)
+
+
+@pytest.mark.parametrize("w", configs.BY_INDEX[:4], ids=lambda w: w.name)
+def test_plan_specialised_source_compiles_with_nvrtc(w):
+    """The plan-specialised likelihood (the tile kernel around the launch's term list,
+    launch-constant rewrite included) compiles to sm_100a SASS with NVRTC, no GPU needed."""
+    m = fb.Model.from_string(w.text)
+    pts = w.points(m, n_points=16)
+    src = fb.plan_spec_source(m, pts, compile=True)
+    nterms = {"c1": 1, "c2": 2, "c3": 3, "c4": 6}[w.name[:2]]
+    assert "struct PlanSpec" in src and f"nterms = {nterms};" in src
+    if w.name.startswith("c2"):
+        # ArgusBG with m0 fixed over the points: the cached kind (plan.hpp LK_ARGUS_CACHED = 8)
+        assert "{8, 0, 1, " in src
+    assert fb.plan_spec_source(m, compile=True)  # the plan without points: as built
+
+
+def test_plan_spec_threshold_switch():
+    old = fb.plan_spec_min_work(-2)
+    try:
+        assert fb.plan_spec_min_work(0) == old
+        assert fb.plan_spec_min_work(-1) == 0
+        assert fb.plan_spec_min_work(-2) == -1
+    finally:
+        fb.plan_spec_min_work(old)
