@@ -217,10 +217,10 @@ int ffcu_expression_jit_source(const ffit_model* m, int compile, char* buf, int 
 /* The build the model's last likelihood launch ran: 0 the static kernels, 1 the
  * formula-specialised build, 2 the plan-specialised build (below). */
 int ffcu_last_launch_jit(const ffit_model* m);
-/* Plan-specialised likelihood builds: launches of more than 8 points and at least
- * FFB_PLAN_SPEC_MIN (default 5e7) event-points of models without Expression pdfs run the
- * tile kernel compiled at run time (NVRTC) around the launch's term list; values as the
- * static build's; FFB_NO_PLAN_SPEC=1 (or ffcu_expression_jit(0)) turns it off.  The
+/* Plan-specialised likelihood builds: launches of at least FFB_PLAN_SPEC_MIN (default 5e7)
+ * event-points of models without Expression pdfs run the tile kernel (or, for <= 8 points
+ * of a single-column single-sum model, the streaming kernel) compiled at run time (NVRTC)
+ * around the launch's term list; values as the static build's; FFB_NO_PLAN_SPEC=1 (or ffcu_expression_jit(0)) turns it off.  The
  * generated source for P points (points may be null: the model's plan as is); compile = 1
  * also NVRTC-compiles it (no GPU needed); at most cap-1 characters into buf. */
 int ffcu_plan_spec_source(ffit_model* m, const double* points, int P, int compile, char* buf, int cap);

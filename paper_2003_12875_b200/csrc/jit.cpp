@@ -706,9 +706,17 @@ namespace {
 
 struct PlanModule {
   CUmodule mod = nullptr;
-  CUfunction fn = nullptr;
-  int occ = 1;
+  CUfunction fn = nullptr;      // tile kernel
+  CUfunction stream = nullptr;  // few-point streaming kernel (single-column single-sum plans)
+  int occ = 1, stream_occ = 1;
 };
+
+bool spec_has_stream(const DevPlan& d) { return d.ncols == 1 && d.simple && d.nderived == 0; }
+
+std::string plan_spec_stream_name(const DevPlan& d, int ks) {
+  return "&ffb::nll_stream_kernel<" + std::to_string(kJitThreads) + ", " + std::to_string(kJitE) + ", 2, " +
+         std::to_string(ks) + ", ffb::PlanSpec>";
+}
 std::map<std::tuple<int, std::string, int>, PlanModule> g_plan_mods;  // (device, source, mode)
 
 int spec_mode(const DevPlan& d, int ks) { return ks + (d.simple ? 0 : 3) + (d.nderived > 0 ? 6 : 0); }
@@ -728,18 +736,26 @@ PlanModule* plan_module(const DevPlan& d, int ks) {
   if (it != g_plan_mods.end()) return it->second.mod ? &it->second : nullptr;
   PlanModule m;  // failures are cached too: no recompile per launch
   DriverApi& drv = driver();
-  const std::string name = plan_spec_kernel_name(d, ks);
+  std::vector<std::string> names = {plan_spec_kernel_name(d, ks)};
+  if (spec_has_stream(d)) names.push_back(plan_spec_stream_name(d, ks));
   std::vector<char> cubin;
   std::vector<std::string> lowered;
   std::string log;
-  if (drv.ok && compile(src, {name}, &cubin, &lowered, &log)) {
+  if (drv.ok && compile(src, names, &cubin, &lowered, &log)) {
     cudaFree(nullptr);
     if (drv.module_load(&m.mod, cubin.data()) == CUDA_SUCCESS &&
-        drv.get_function(&m.fn, m.mod, lowered[0].c_str()) == CUDA_SUCCESS) {
+        drv.get_function(&m.fn, m.mod, lowered[0].c_str()) == CUDA_SUCCESS &&
+        (names.size() < 2 || drv.get_function(&m.stream, m.mod, lowered[1].c_str()) == CUDA_SUCCESS)) {
       drv.set_attribute(m.fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
                         kMaxCols * kJitTile * static_cast<int>(sizeof(double)));
       drv.occupancy(&m.occ, m.fn, kJitThreads, (d.ncols + 2 * d.nderived) * kJitTile * sizeof(double));
       if (m.occ < 1) m.occ = 1;
+      if (m.stream) {
+        const int ss = kJitStages * kJitTile * static_cast<int>(sizeof(double));
+        drv.set_attribute(m.stream, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, ss);
+        drv.occupancy(&m.stream_occ, m.stream, kJitThreads, ss);
+        if (m.stream_occ < 1) m.stream_occ = 1;
+      }
     } else {
       m.mod = nullptr;
     }
@@ -785,8 +801,9 @@ double plan_spec_min_work(double v) {
 
 bool plan_spec_applies(const HostPlan& plan, const DevPlan& launch, long long n, int P) {
   const double min_work = g_spec_min.load();
-  if (min_work < 0.0 || !jit_enabled() || !plan.programs.empty()) return false;
-  if (P <= kJitStreamMaxP || launch.nterms < 1) return false;  // the streaming build serves few points
+  if (min_work < 0.0 || !jit_enabled() || !plan.programs.empty() || launch.nterms < 1) return false;
+  // few-point launches of multi-column or product plans: the static tile kernel
+  if (P <= kJitStreamMaxP && !spec_has_stream(launch)) return false;
   return static_cast<double>(n) * P >= min_work;
 }
 
@@ -795,7 +812,9 @@ bool plan_spec_prepare(const DevPlan& launch, int ks) { return plan_module(launc
 bool plan_spec_compile_only(const DevPlan& launch, int ks, std::string* log) {
   std::vector<char> cubin;
   std::vector<std::string> low;
-  return compile(plan_spec_source(launch), {plan_spec_kernel_name(launch, ks)}, &cubin, &low, log);
+  std::vector<std::string> names = {plan_spec_kernel_name(launch, ks)};
+  if (spec_has_stream(launch)) names.push_back(plan_spec_stream_name(launch, ks));
+  return compile(plan_spec_source(launch), names, &cubin, &low, log);
 }
 
 NllLaunchInfo launch_nll_spec(const DevPlan& launch, const ColPtrs& cols, long long n, const double* d_consts, int P,
@@ -817,6 +836,29 @@ NllLaunchInfo launch_nll_spec(const DevPlan& launch, const ColPtrs& cols, long l
   long long ntl = (n + kJitTile - 1) / kJitTile;
   if (ntl < 1) ntl = 1;
   int ntiles = static_cast<int>(ntl);
+  if (m->stream && P <= kJitStreamMaxP && (reinterpret_cast<uintptr_t>(cols.c[0]) & 15) == 0 &&
+      std::getenv("FFB_NO_STREAM") == nullptr) {
+    // few points: the persistent streaming kernel (kernels_device.cuh nll_stream_kernel)
+    long long G = static_cast<long long>(device_sm_count()) * m->stream_occ;
+    if (G > ntl) G = ntl;
+    void* sargs[] = {&dp, &cp, &nn, &kc, &PP, &ntiles, &partial, &bad};
+    if (ev_start) cudaEventRecord(ev_start, stream);
+    const CUresult rc = drv.launch(m->stream, static_cast<unsigned>(G), 1, 1, kJitThreads, 1, 1,
+                                   kJitStages * kJitTile * sizeof(double), reinterpret_cast<CUstream>(stream), sargs,
+                                   nullptr);
+    if (ev_stop) cudaEventRecord(ev_stop, stream);
+    if (rc != CUDA_SUCCESS) numeric_error("cuLaunchKernel (plan-specialised likelihood) failed: " + std::to_string(rc));
+    launch_reduce(partial, static_cast<int>(G), P, d_out, stream);
+    info.threads = kJitThreads;
+    info.events_per_thread = kJitE;
+    info.tile = kJitTile;
+    info.ntiles = ntiles;
+    info.nchunks = 0;
+    info.grid = static_cast<int>(G);
+    info.launches = 2;
+    info.jit = 2;
+    return info;
+  }
   // the static builds' grid rule (kernels.cu nll_shape): >= `waves` waves of resident CTAs
   const long long slots = static_cast<long long>(device_sm_count()) * m->occ;
   long long want = (waves * slots + ntiles - 1) / ntiles;

@@ -51,9 +51,10 @@ NllLaunchInfo launch_nll_grad_spec(const HostPlan& plan, const GradPlan& gp, con
 
 // Plan-specialised likelihood builds (kernels_device.cuh eval_plan_spec): the tile
 // kernel compiled at run time around the launch's term list (kinds, columns, flags,
-// constant offsets as compile-time constants; the launch-constant rewrite included), for
-// launches of more than kStreamMaxP points and at least FFB_PLAN_SPEC_MIN (default 5e7)
-// event-points; models without Expression leaves.  FFB_NO_PLAN_SPEC=1 turns it off.
+// constant offsets as compile-time constants; the launch-constant rewrite included), and
+// for single-column single-sum plans the few-point streaming kernel the same way; for
+// launches of at least FFB_PLAN_SPEC_MIN (default 5e7) event-points of models without
+// Expression leaves.  FFB_NO_PLAN_SPEC=1 turns it off.
 std::string plan_spec_source(const DevPlan& launch);
 // Sets the event-point threshold (v >= 0; -1 turns the builds off; other negatives only
 // query); returns the previous setting.

@@ -648,13 +648,18 @@ def test_plan_specialised_build_matches_static_build(name):
     try:
         static, sbad, _ = fb.nll_points(m, ds, pts)
         assert fb.last_launch_jit(m) == 0
+        few, _, _ = fb.nll_points(m, ds, pts[:3])  # the streaming build where one exists
         fb.plan_spec_min_work(0)
         spec, bad, _ = fb.nll_points(m, ds, pts)
         assert fb.last_launch_jit(m) == 2, fb.expression_jit_status()
+        few_spec, _, _ = fb.nll_points(m, ds, pts[:3])
+        if len(m.observables) == 1:  # single-column single-sum: the specialised streaming kernel
+            assert fb.last_launch_jit(m) == 2
     finally:
         fb.plan_spec_min_work(old)
     assert np.array_equal(bad, sbad)
     assert np.array_equal(spec, static), np.max(np.abs(spec - static) / np.abs(static))
+    assert np.array_equal(few_spec, few), np.max(np.abs(few_spec - few) / np.abs(few))
     for p in (0, 11):
         _, comp, ob = o.nll(cols, pts[p])
         assert bad[p] == ob
