@@ -177,9 +177,15 @@ bool compile(const std::string& source, const std::vector<std::string>& names, s
     return false;
   }
   for (const auto& n : names) api.add_name(prog, n.c_str());
-  const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo",
-                        "--device-as-default-execution-space", "-diag-suppress=128"};
-  const nvrtcResult rc = api.compile(prog, 5, opts);
+  std::vector<std::string> extra;  // FFB_JIT_OPTS: extra NVRTC options (A/B builds, e.g. -DFFB_CONST_BANK)
+  if (const char* e = std::getenv("FFB_JIT_OPTS")) {
+    std::istringstream is(e);
+    for (std::string w; is >> w;) extra.push_back(w);
+  }
+  std::vector<const char*> opts = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo",
+                                   "--device-as-default-execution-space", "-diag-suppress=128"};
+  for (const auto& w : extra) opts.push_back(w.c_str());
+  const nvrtcResult rc = api.compile(prog, static_cast<int>(opts.size()), opts.data());
   std::size_t ls = 0;
   api.log_size(prog, &ls);
   std::string l(ls, '\0');
@@ -770,7 +776,11 @@ PlanModule* plan_module(const DevPlan& d, int ks) {
 
 std::string plan_spec_source(const DevPlan& d) {
   std::ostringstream o;
+  // FFB_CONST_BANK: the exp / log polynomial constants as constant-bank DFMA operands
+  // instead of 64-bit immediates materialised per use (A/B, profiles/r01_ab1: +0.2-2.3 %
+  // on C2-C4, -0.5 % on C1)
   o << "// generated by jit.cpp: the launch's term list for nll_kernel<..., PlanSpec>\n"
+       "#define FFB_CONST_BANK 1\n"
        "#include \"plan.hpp\"\nnamespace ffb {\nstruct PlanSpec {\n"
        "  static constexpr bool kOn = true;\n"
     << "  static constexpr int nterms = " << d.nterms << ";\n"
