@@ -214,6 +214,10 @@ const char* ffcu_expression_jit_status(void);
 /* The generated formula source of a model (compile = 1: also NVRTC-compile the kernels
  * around it, no GPU needed); at most cap-1 characters into buf. */
 int ffcu_expression_jit_source(const ffit_model* m, int compile, char* buf, int cap);
+/* The same for a launch over P points: formula subtrees whose inputs (x, constants,
+ * parameters) are identical over all the points are computed once per staged tile
+ * (launch-constant cache) and the generated source shows them (ffb_expr_hoist). */
+int ffcu_expression_jit_source_points(ffit_model* m, const double* points, int P, int compile, char* buf, int cap);
 /* The build the model's last likelihood launch ran: 0 the static kernels, 1 the
  * formula-specialised build, 2 the plan-specialised build (below). */
 int ffcu_last_launch_jit(const ffit_model* m);

@@ -92,6 +92,7 @@ SIGNATURES = {
     "ffcu_last_launch_cached": (I, [VP]),
     "ffcu_plan_spec_source": (I, [VP, DP, I, I, ctypes.c_char_p, I]),
     "ffcu_plan_spec_min_work": (ctypes.c_double, [ctypes.c_double]),
+    "ffcu_expression_jit_source_points": (I, [VP, DP, I, I, ctypes.c_char_p, I]),
     "ffcu_grad_spec_source": (I, [VP, I, CP, I]),
     "ffcu_last_grad_jit": (I, [VP]),
     "ffcu_soa_write": (I, [CP, ctypes.POINTER(CP), ctypes.POINTER(DP), I, LL]),

@@ -640,6 +640,35 @@ FFB_API int ffcu_expression_jit_source(const ffit_model* m, int compile, char* b
   });
 }
 
+FFB_API int ffcu_expression_jit_source_points(ffit_model* m, const double* points, int P, int compile, char* buf,
+                                              int cap) {
+  return guarded([&] {
+    require(m, "model");
+    require(points, "points");
+    const ffb::HostPlan& plan = engine(m).likelihood_plan();
+    if (plan.programs.empty()) ffb::usage_error("the model has no Expression pdf");
+    const std::size_t npar = m->m->params.size();
+    std::vector<double> rows(static_cast<std::size_t>(P > 0 ? P : 0) * plan.dev.stride);
+    for (int p = 0; p < P; ++p) {
+      ffb::build_constants(plan, *m->m, points + p * npar, rows.data() + static_cast<std::size_t>(p) * plan.dev.stride,
+                           std::ldexp(1.0, ffb::kPScaleLog2));
+    }
+    const ffb::ExprHoist hoist = ffb::analyse_expr_hoist(plan, rows.data(), P);
+    const std::string text = ffb::jit_expression_source(plan, &hoist);
+    if (compile) {
+      std::string log;
+      if (!ffb::jit_compile_only(plan, &log, &hoist)) {
+        ffb::numeric_error("NVRTC compile of the formula-specialised kernels failed: " + log.substr(0, 4000));
+      }
+    }
+    if (buf && cap > 0) {
+      const std::size_t k = std::min<std::size_t>(text.size(), static_cast<std::size_t>(cap - 1));
+      std::memcpy(buf, text.data(), k);
+      buf[k] = '\0';
+    }
+  });
+}
+
 FFB_API int ffcu_last_launch_jit(const ffit_model* m) { return m && m->engine ? m->engine->last_launch().jit : 0; }
 
 FFB_API double ffcu_plan_spec_min_work(double v) { return ffb::plan_spec_min_work(v); }

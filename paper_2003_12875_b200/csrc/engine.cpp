@@ -308,7 +308,7 @@ int Engine::nll_points_device(const DeviceDataset& ds, const double* thetas, int
     }
     if (!plan_.programs.empty() && jit_prepare(plan_)) {
       // Expression leaves: the formula-specialised build (jit.cpp) instead of the interpreter
-      last_ = launch_nll_jit(plan_, cols, ds.n, d_consts, P, d_scratch_, d_pairs, d_bad, s, ea, eb);
+      last_ = launch_nll_jit(plan_, cols, ds.n, d_consts, P, d_scratch_, d_pairs, d_bad, s, h_consts_[slot_], ea, eb);
     } else {
       // launch-constant branches (ArgusBG with m0 fixed over the launch) cached per tile
       DevPlan lp = plan_.dev;

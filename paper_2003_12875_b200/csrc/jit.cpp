@@ -19,6 +19,8 @@
 
 namespace ffb {
 
+std::string plan_spec_struct(const DevPlan& d);
+
 namespace {
 
 #include "jit_sources.inc"  // kJitHeaders: the device headers as strings (embed_sources.py)
@@ -121,6 +123,7 @@ struct Module {
   CUfunction tile = nullptr;
   CUfunction stream = nullptr;  // single-column single-sum plans only
   int tile_occ = 1, stream_occ = 1;
+  int smem_cols = 1;  // data columns + cached formula subtrees
 };
 std::map<std::pair<int, std::string>, Module> g_modules;  // (device, source)
 
@@ -145,15 +148,17 @@ int jit_kind_set(const HostPlan& plan) {
   return ks;
 }
 
-std::string tile_name(const HostPlan& plan) {
+// formula builds are plan-specialised too (PlanSpec); MODE + 6 (the launch-constant
+// builds) when the launch caches formula subtrees
+std::string tile_name(const HostPlan& plan, bool hoisted) {
   const bool onecol = plan.dev.ncols == 1;
-  const int mode = jit_kind_set(plan) + (plan.dev.simple ? 0 : 3);
+  const int mode = jit_kind_set(plan) + (plan.dev.simple ? 0 : 3) + (hoisted ? 6 : 0);
   return "&ffb::nll_kernel<" + std::to_string(kJitThreads) + ", " + std::to_string(kJitE) + ", " +
-         (onecol ? "true" : "false") + ", 2, " + std::to_string(mode) + ">";
+         (onecol ? "true" : "false") + ", 2, " + std::to_string(mode) + ", ffb::PlanSpec>";
 }
 std::string stream_name(const HostPlan& plan) {
   return "&ffb::nll_stream_kernel<" + std::to_string(kJitThreads) + ", " + std::to_string(kJitE) + ", 2, " +
-         std::to_string(jit_kind_set(plan)) + ">";
+         std::to_string(jit_kind_set(plan)) + ", ffb::PlanSpec>";
 }
 bool has_stream(const HostPlan& plan) { return plan.dev.ncols == 1 && plan.dev.simple; }
 
@@ -221,13 +226,228 @@ bool compile(const std::string& source, const std::vector<std::string>& names, s
   return ok;
 }
 
-std::string full_source(const HostPlan& plan) {
-  return jit_expression_source(plan) + "#include \"kernels_device.cuh\"\n";
+// ---------------------------------------------------------------------------
+// formula code generation (jit_expression_source)
+
+// Emits the stack code of program instructions [b, e) as a scoped block whose value ends
+// in the E-array `result`.  Ranges listed in `hoisted` (launch-constant subtrees) push
+// their cached shared-memory column instead of being computed.
+void emit_block(std::ostream& o, const std::vector<ExprInstr>& prog, int b, int e,
+                const std::vector<const HoistSlot*>* hoisted, const std::string& result) {
+  int depth = 0, max_depth = 0;
+  std::ostringstream body;
+  std::vector<bool> uni(kExprMaxDepth + 2, false);  // the slot holds one value for every event
+  auto S = [](int d) { return "s" + std::to_string(d); };
+  // a uniform slot is a scalar u<d>; the others are arrays s<d>[E]
+  auto U = [](int d) { return "u" + std::to_string(d); };
+  auto elem = [&](int d) { return uni[d] ? U(d) : S(d) + "[e]"; };
+  auto loop = [&](const std::string& stmt) {
+    body << "#pragma unroll\n  for (int e = 0; e < E; ++e) " << stmt << "\n";
+  };
+  auto widen = [&](int d) {  // make slot d an array (before a per-event op writes it)
+    if (uni[d]) {
+      loop(S(d) + "[e] = " + U(d) + ";");
+      uni[d] = false;
+    }
+  };
+  for (int j = b; j < e; ++j) {
+    const HoistSlot* h = nullptr;
+    if (hoisted) {
+      for (const HoistSlot* c : *hoisted) h = c->begin == j ? c : h;
+    }
+    if (h) {  // the whole subtree [begin, end] from the tile's cache
+      loop(S(depth) + "[e] = dsm[" + std::to_string(h->col) + " * (T * E) + e * T];");
+      uni[depth] = false;
+      ++depth;
+      if (depth > max_depth) max_depth = depth;
+      j = h->end;
+      continue;
+    }
+    const ExprInstr& in = prog[j];
+    switch (in.op) {
+      case EX_CONST:
+        body << "  " << U(depth) << " = " << hexbits(in.c) << ";\n";
+        uni[depth] = true;
+        ++depth;
+        break;
+      case EX_VAR:
+        body << "  " << U(depth) << " = k[" << 1 + in.slot << "];\n";
+        uni[depth] = true;
+        ++depth;
+        break;
+      case EX_X:
+        loop(S(depth) + "[e] = x[e];");
+        uni[depth] = false;
+        ++depth;
+        break;
+      case EX_ADD: case EX_SUB: case EX_MUL: case EX_POW: case EX_DIV: {
+        --depth;
+        const int l = depth - 1, r = depth;
+        const char* fn = in.op == EX_ADD ? "__dadd_rn" : in.op == EX_SUB ? "__dsub_rn" : in.op == EX_MUL ? "__dmul_rn"
+                       : in.op == EX_POW ? "ffb_pow" : "__ddiv_rn";
+        if (uni[l] && uni[r]) {  // both uniform: a scalar (the compiler computes it once)
+          body << "  " << U(l) << " = " << fn << "(" << U(l) << ", " << U(r) << ");\n";
+        } else if (in.op == EX_DIV && uni[r]) {
+          body << "  ffb_vdiv_uniform<E>(" << S(l) << ", " << U(r) << ");\n";
+        } else if (in.op == EX_DIV) {
+          widen(l);
+          widen(r);
+          body << "  ffb_vdiv<E>(" << S(l) << ", " << S(r) << ");\n";
+        } else {
+          const std::string lhs = elem(l), rhs = elem(r);
+          loop(S(l) + "[e] = " + fn + "(" + lhs + ", " + rhs + ");");
+          uni[l] = false;
+        }
+        break;
+      }
+      default: {  // unary
+        const int d = depth - 1;
+        if (uni[d]) {  // a uniform operand stays scalar: libdevice / IEEE, computed once
+          const char* f = in.op == EX_NEG ? "-" : in.op == EX_EXP ? "exp" : in.op == EX_LOG ? "log"
+                        : in.op == EX_SIN ? "sin" : in.op == EX_COS ? "cos" : in.op == EX_SQRT ? "__dsqrt_rn"
+                        : in.op == EX_ABS ? "fabs" : in.op == EX_SINH ? "sinh" : in.op == EX_ASINH ? "asinh"
+                        : nullptr;
+          if (in.op == EX_SQUARE) {
+            body << "  " << U(d) << " = __dmul_rn(" << U(d) << ", " << U(d) << ");\n";
+          } else if (in.op == EX_CUBE) {
+            body << "  " << U(d) << " = __dmul_rn(__dmul_rn(" << U(d) << ", " << U(d) << "), " << U(d) << ");\n";
+          } else if (in.op == EX_FOURTH) {
+            body << "  { const double t = __dmul_rn(" << U(d) << ", " << U(d) << "); " << U(d)
+                 << " = __dmul_rn(t, t); }\n";
+          } else {
+            body << "  " << U(d) << " = " << f << "(" << U(d) << ");\n";
+          }
+          break;
+        }
+        const std::string a = S(d) + "[e]";
+        switch (in.op) {
+          case EX_NEG: loop(a + " = -" + a + ";"); break;
+          case EX_SQUARE: loop(a + " = __dmul_rn(" + a + ", " + a + ");"); break;
+          case EX_CUBE: loop(a + " = __dmul_rn(__dmul_rn(" + a + ", " + a + "), " + a + ");"); break;
+          case EX_FOURTH: loop("{ const double t = __dmul_rn(" + a + ", " + a + "); " + a + " = __dmul_rn(t, t); }"); break;
+          case EX_EXP: body << "  ffb_vexp<E>(" << S(d) << ", tb);\n"; break;
+          case EX_LOG: body << "  ffb_vlog<E>(" << S(d) << ", tb);\n"; break;
+          case EX_SQRT: body << "  ffb_vsqrt<E>(" << S(d) << ");\n"; break;
+          case EX_ABS: loop(a + " = fabs(" + a + ");"); break;
+          case EX_SIN: loop(a + " = sin(" + a + ");"); break;
+          case EX_COS: loop(a + " = cos(" + a + ");"); break;
+          case EX_SINH: loop(a + " = sinh(" + a + ");"); break;
+          default: loop(a + " = asinh(" + a + ");"); break;
+        }
+        break;
+      }
+    }
+    if (depth > max_depth) max_depth = depth;
+  }
+  o << "  {\n";
+  for (int d = 0; d < max_depth; ++d) o << "  double s" << d << "[E];\n  double u" << d << ";\n";
+  o << body.str();
+  if (uni[0]) {
+    o << "#pragma unroll\n  for (int e = 0; e < E; ++e) " << result << "[e] = u0;\n";
+  } else {
+    o << "#pragma unroll\n  for (int e = 0; e < E; ++e) " << result << "[e] = s0[e];\n";
+  }
+  o << "  }\n";
+}
+
+int program_end(const std::vector<ExprInstr>& prog, int off) {
+  int j = off;
+  while (prog[j].op != EX_END) ++j;
+  return j;
+}
+
+// One formula function: `name`(x, k, v, tb) or, with hoisted ranges, name<E, T>(..., dsm).
+void emit_formula(std::ostream& o, const std::vector<ExprInstr>& prog, int off,
+                  const std::vector<const HoistSlot*>* hoisted, const std::string& name, bool with_dsm) {
+  if (with_dsm) {
+    o << "template <int E, int T>\n__device__ __forceinline__ void " << name
+      << "(const double (&x)[E], const double* __restrict__ k, double (&v)[E], const MathTables* __restrict__ tb,\n"
+         "    const double* __restrict__ dsm) {\n  (void)x; (void)k; (void)tb; (void)dsm;\n";
+  } else {
+    o << "template <int E>\n__device__ __forceinline__ void " << name
+      << "(const double (&x)[E], const double* __restrict__ k, double (&v)[E], const MathTables* __restrict__ tb) {\n"
+      << "  (void)x; (void)k; (void)tb;\n";
+  }
+  emit_block(o, prog, off, program_end(prog, off), hoisted, "v");
+  o << "}\n";
 }
 
 }  // namespace
 
-std::string jit_expression_source(const HostPlan& plan) {
+ExprHoist analyse_expr_hoist(const HostPlan& plan, const double* rows, int P) {
+  ExprHoist out;
+  if (!rows || P < 2) return out;
+  const DevPlan& d = plan.dev;
+  int next_col = d.ncols + 2 * d.nderived;
+  auto bits = [](double v) {
+    unsigned long long b;
+    std::memcpy(&b, &v, sizeof b);
+    return b;
+  };
+  for (int i = 0; i < d.nterms; ++i) {
+    const DevTerm& t = d.t[i];
+    if (t.kind != LK_EXPR) continue;
+    int users = 0;
+    for (int k = 0; k < d.nterms; ++k) users += (d.t[k].kind == LK_EXPR && d.t[k].order == t.order) ? 1 : 0;
+    if (users != 1) continue;  // a program shared by several terms: not cached (per-term columns)
+    const int off = t.order, end = program_end(plan.programs, off);
+    const int n = end - off;
+    std::vector<int> start(n), parent(n, -1), cost(n, 0);
+    std::vector<char> inv(n, 0), hasx(n, 0);
+    std::vector<int> st;
+    auto uniform = [&](int slot) {
+      const double* k0 = rows + t.coff + 1 + slot;
+      for (int p = 1; p < P; ++p) {
+        if (bits(k0[static_cast<std::size_t>(p) * d.stride]) != bits(*k0)) return false;
+      }
+      return true;
+    };
+    for (int j = 0; j < n; ++j) {
+      const ExprInstr& in = plan.programs[off + j];
+      switch (in.op) {
+        case EX_CONST: start[j] = j; inv[j] = 1; st.push_back(j); break;
+        case EX_VAR: start[j] = j; inv[j] = uniform(in.slot) ? 1 : 0; st.push_back(j); break;
+        case EX_X: start[j] = j; inv[j] = 1; hasx[j] = 1; st.push_back(j); break;
+        case EX_ADD: case EX_SUB: case EX_MUL: case EX_POW: case EX_DIV: {
+          const int r = st.back(); st.pop_back();
+          const int l = st.back(); st.pop_back();
+          parent[l] = parent[r] = j;
+          start[j] = start[l];
+          inv[j] = inv[l] && inv[r];
+          hasx[j] = hasx[l] || hasx[r];
+          cost[j] = cost[l] + cost[r] + ((in.op == EX_POW || in.op == EX_DIV) ? 8 : 1);
+          st.push_back(j);
+          break;
+        }
+        default: {
+          const int c = st.back(); st.pop_back();
+          parent[c] = j;
+          start[j] = start[c];
+          inv[j] = inv[c];
+          hasx[j] = hasx[c];
+          const bool heavy = in.op == EX_EXP || in.op == EX_LOG || in.op == EX_SQRT || in.op == EX_SIN ||
+                             in.op == EX_COS || in.op == EX_SINH || in.op == EX_ASINH;
+          cost[j] = cost[c] + (heavy ? 8 : 1);
+          st.push_back(j);
+          break;
+        }
+      }
+    }
+    for (int j = 0; j < n; ++j) {
+      const bool maximal = parent[j] < 0 || !inv[parent[j]];
+      if (!inv[j] || !hasx[j] || !maximal || cost[j] < 3) continue;  // x alone / cheap: not worth a column
+      if (next_col >= kMaxCols) break;
+      out.slots.push_back(HoistSlot{i, off, off + start[j], off + j, next_col++, t.col, t.coff});
+    }
+  }
+  return out;
+}
+
+namespace {
+
+}  // namespace
+
+std::string jit_expression_source(const HostPlan& plan, const ExprHoist* hoist) {
   // Each formula becomes code over the thread's E events at once (one array per stack
   // depth, every operation an unrolled loop), so the compiler interleaves the events.
   // exp / log / sqrt / division take branch-free fast forms (fastmath.cuh, <= 2 ulp; the
@@ -321,6 +541,11 @@ std::string jit_expression_source(const HostPlan& plan) {
        "#pragma unroll\n"
        "  for (int e = 0; e < E; ++e) a[e] = r[e];\n"
        "}\n";
+  // per program offset: the hoisted ranges (launch-constant subtrees, ExprHoist)
+  std::map<int, std::vector<const HoistSlot*>> by_prog;
+  if (hoist) {
+    for (const HoistSlot& h : hoist->slots) by_prog[h.prog].push_back(&h);
+  }
   std::vector<int> offsets;
   for (int i = 0; i < plan.dev.nterms; ++i) {
     if (plan.dev.t[i].kind != LK_EXPR) continue;
@@ -329,117 +554,51 @@ std::string jit_expression_source(const HostPlan& plan) {
     for (const int sv : offsets) seen = seen || sv == off;
     if (seen) continue;
     offsets.push_back(off);
-    int depth = 0, max_depth = 0;
-    std::ostringstream body;
-    std::vector<bool> uni(kExprMaxDepth + 1, false);  // the slot holds one value for every event
-    auto S = [](int d) { return "s" + std::to_string(d); };
-    // a uniform slot is a scalar u<d>; the others are arrays s<d>[E]
-    auto U = [](int d) { return "u" + std::to_string(d); };
-    auto elem = [&](int d) { return uni[d] ? U(d) : S(d) + "[e]"; };
-    auto loop = [&](const std::string& stmt) {
-      body << "#pragma unroll\n  for (int e = 0; e < E; ++e) " << stmt << "\n";
-    };
-    auto widen = [&](int d) {  // make slot d an array (before a per-event op writes it)
-      if (uni[d]) {
-        loop(S(d) + "[e] = " + U(d) + ";");
-        uni[d] = false;
-      }
-    };
-    for (std::size_t j = static_cast<std::size_t>(off); plan.programs[j].op != EX_END; ++j) {
-      const ExprInstr& in = plan.programs[j];
-      switch (in.op) {
-        case EX_CONST:
-          body << "  " << U(depth) << " = " << hexbits(in.c) << ";\n";
-          uni[depth] = true;
-          ++depth;
-          break;
-        case EX_VAR:
-          body << "  " << U(depth) << " = k[" << 1 + in.slot << "];\n";
-          uni[depth] = true;
-          ++depth;
-          break;
-        case EX_X:
-          loop(S(depth) + "[e] = x[e];");
-          uni[depth] = false;
-          ++depth;
-          break;
-        case EX_ADD: case EX_SUB: case EX_MUL: case EX_POW: case EX_DIV: {
-          --depth;
-          const int l = depth - 1, r = depth;
-          const char* fn = in.op == EX_ADD ? "__dadd_rn" : in.op == EX_SUB ? "__dsub_rn" : in.op == EX_MUL ? "__dmul_rn"
-                         : in.op == EX_POW ? "ffb_pow" : "__ddiv_rn";
-          if (uni[l] && uni[r]) {  // both uniform: a scalar (the compiler computes it once)
-            body << "  " << U(l) << " = " << fn << "(" << U(l) << ", " << U(r) << ");\n";
-          } else if (in.op == EX_DIV && uni[r]) {
-            body << "  ffb_vdiv_uniform<E>(" << S(l) << ", " << U(r) << ");\n";
-          } else if (in.op == EX_DIV) {
-            widen(l);
-            widen(r);
-            body << "  ffb_vdiv<E>(" << S(l) << ", " << S(r) << ");\n";
-          } else {
-            const std::string lhs = elem(l), rhs = elem(r);
-            loop(S(l) + "[e] = " + fn + "(" + lhs + ", " + rhs + ");");
-            uni[l] = false;
-          }
-          break;
-        }
-        default: {  // unary
-          const int d = depth - 1;
-          if (uni[d]) {  // a uniform operand stays scalar: libdevice / IEEE, computed once
-            const char* f = in.op == EX_NEG ? "-" : in.op == EX_EXP ? "exp" : in.op == EX_LOG ? "log"
-                          : in.op == EX_SIN ? "sin" : in.op == EX_COS ? "cos" : in.op == EX_SQRT ? "__dsqrt_rn"
-                          : in.op == EX_ABS ? "fabs" : in.op == EX_SINH ? "sinh" : in.op == EX_ASINH ? "asinh"
-                          : nullptr;
-            if (in.op == EX_SQUARE) {
-              body << "  " << U(d) << " = __dmul_rn(" << U(d) << ", " << U(d) << ");\n";
-            } else if (in.op == EX_CUBE) {
-              body << "  " << U(d) << " = __dmul_rn(__dmul_rn(" << U(d) << ", " << U(d) << "), " << U(d) << ");\n";
-            } else if (in.op == EX_FOURTH) {
-              body << "  { const double t = __dmul_rn(" << U(d) << ", " << U(d) << "); " << U(d)
-                   << " = __dmul_rn(t, t); }\n";
-            } else {
-              body << "  " << U(d) << " = " << f << "(" << U(d) << ");\n";
-            }
-            break;
-          }
-          const std::string a = S(d) + "[e]";
-          switch (in.op) {
-            case EX_NEG: loop(a + " = -" + a + ";"); break;
-            case EX_SQUARE: loop(a + " = __dmul_rn(" + a + ", " + a + ");"); break;
-            case EX_CUBE: loop(a + " = __dmul_rn(__dmul_rn(" + a + ", " + a + "), " + a + ");"); break;
-            case EX_FOURTH: loop("{ const double t = __dmul_rn(" + a + ", " + a + "); " + a + " = __dmul_rn(t, t); }"); break;
-            case EX_EXP: body << "  ffb_vexp<E>(" << S(d) << ", tb);\n"; break;
-            case EX_LOG: body << "  ffb_vlog<E>(" << S(d) << ", tb);\n"; break;
-            case EX_SQRT: body << "  ffb_vsqrt<E>(" << S(d) << ");\n"; break;
-            case EX_ABS: loop(a + " = fabs(" + a + ");"); break;
-            case EX_SIN: loop(a + " = sin(" + a + ");"); break;
-            case EX_COS: loop(a + " = cos(" + a + ");"); break;
-            case EX_SINH: loop(a + " = sinh(" + a + ");"); break;
-            default: loop(a + " = asinh(" + a + ");"); break;
-          }
-          break;
-        }
-      }
-      if (depth > max_depth) max_depth = depth;
+    emit_formula(o, plan.programs, off, nullptr, "ffb_expr_" + std::to_string(off), false);
+    auto it = by_prog.find(off);
+    if (it != by_prog.end()) {
+      emit_formula(o, plan.programs, off, &it->second, "ffb_expr_" + std::to_string(off) + "_h", true);
     }
-    o << "template <int E>\n__device__ __forceinline__ void ffb_expr_" << off
-      << "(const double (&x)[E], const double* __restrict__ k, double (&v)[E], const MathTables* __restrict__ tb) {\n"
-      << "  (void)x; (void)k; (void)tb;\n";
-    for (int d = 0; d < max_depth; ++d) o << "  double s" << d << "[E];\n  double u" << d << ";\n";
-    o << body.str();
-    if (uni[0]) {
-      o << "#pragma unroll\n  for (int e = 0; e < E; ++e) v[e] = u0;\n";
-    } else {
-      o << "#pragma unroll\n  for (int e = 0; e < E; ++e) v[e] = s0[e];\n";
-    }
-    o << "}\n";
   }
   o << "template <int E>\n"
        "__device__ __forceinline__ void ffb_expr_batch(int off, const double* __restrict__ k, const double (&x)[E],\n"
        "                                               double (&v)[E], const MathTables* __restrict__ tb) {\n"
        "  switch (off) {\n";
   for (const int off : offsets) o << "    case " << off << ": ffb_expr_" << off << "<E>(x, k, v, tb); break;\n";
-  o << "    default: break;\n  }\n}\n}  // namespace ffb\n";
+  o << "    default: break;\n  }\n}\n";
+  if (hoist && !hoist->slots.empty()) {
+    // the launch-constant subtrees: computed once per staged tile (nll_kernel) into
+    // shared-memory columns, read by the _h formulas for every point
+    o << "#define FFB_EXPR_HOIST 1\n"
+         "template <int E, int T>\n"
+         "__device__ __forceinline__ void ffb_expr_batch_h(int off, const double* __restrict__ k, const double (&x)[E],\n"
+         "                                                 double (&v)[E], const MathTables* __restrict__ tb,\n"
+         "                                                 const double* __restrict__ dsm) {\n"
+         "  (void)dsm;\n  switch (off) {\n";
+    for (const int off : offsets) {
+      if (by_prog.count(off)) {
+        o << "    case " << off << ": ffb_expr_" << off << "_h<E, T>(x, k, v, tb, dsm); break;\n";
+      } else {
+        o << "    case " << off << ": ffb_expr_" << off << "<E>(x, k, v, tb); break;\n";
+      }
+    }
+    o << "    default: break;\n  }\n}\n";
+    o << "template <int E, int T>\n"
+         "__device__ __forceinline__ void ffb_expr_hoist(const double* __restrict__ row, double* __restrict__ dsm,\n"
+         "                                               const MathTables* __restrict__ tb) {\n"
+         "  (void)tb;\n";
+    for (const HoistSlot& h : hoist->slots) {
+      o << "  {  // column " << h.col << ": program " << h.prog << " instructions [" << h.begin << ", " << h.end
+        << "] of term " << h.term << "\n"
+        << "    const double* __restrict__ k = row + " << h.coff << ";\n    double x[E];\n"
+        << "#pragma unroll\n    for (int e = 0; e < E; ++e) x[e] = dsm[" << h.xcol << " * (T * E) + e * T];\n"
+        << "    double r[E];\n";
+      emit_block(o, plan.programs, h.begin, h.end + 1, nullptr, "r");
+      o << "#pragma unroll\n    for (int e = 0; e < E; ++e) dsm[" << h.col << " * (T * E) + e * T] = r[e];\n  }\n";
+    }
+    o << "}\n";
+  }
+  o << "}  // namespace ffb\n";
   return o.str();
 }
 
@@ -580,27 +739,42 @@ std::string jit_status() {
   return g_status;
 }
 
-bool jit_compile_only(const HostPlan& plan, std::string* log) {
-  std::vector<std::string> names = {tile_name(plan)};
+namespace {
+
+// formula builds: the generated formulas (with the launch's cached subtrees), the plan's
+// term list (PlanSpec) and the fused kernels
+std::string full_source(const HostPlan& plan, const ExprHoist* hoist) {
+  return "#define FFB_CONST_BANK 1\n" + jit_expression_source(plan, hoist) + plan_spec_struct(plan.dev) +
+         "#include \"kernels_device.cuh\"\n";
+}
+
+int hoist_cols(const ExprHoist* hoist) { return hoist ? static_cast<int>(hoist->slots.size()) : 0; }
+
+}  // namespace
+
+bool jit_compile_only(const HostPlan& plan, std::string* log, const ExprHoist* hoist) {
+  const bool h = hoist_cols(hoist) > 0;
+  std::vector<std::string> names = {tile_name(plan, h)};
   if (has_stream(plan)) names.push_back(stream_name(plan));
   std::vector<char> cubin;
   std::vector<std::string> low;
-  return compile(full_source(plan), names, &cubin, &low, log);
+  return compile(full_source(plan, hoist), names, &cubin, &low, log);
 }
 
 namespace {
 
-Module* module_for(const HostPlan& plan) {
+Module* module_for(const HostPlan& plan, const ExprHoist* hoist) {
   int dev = 0;
   cudaGetDevice(&dev);
-  const std::string src = full_source(plan);
+  const std::string src = full_source(plan, hoist);
   const auto key = std::make_pair(dev, src);
   std::lock_guard<std::mutex> lk(g_mu);
   auto it = g_modules.find(key);
   if (it != g_modules.end()) return it->second.mod ? &it->second : nullptr;
   Module m;  // a failed compile is cached too (mod stays null): no retry per launch
   DriverApi& drv = driver();
-  std::vector<std::string> names = {tile_name(plan)};
+  const int hc = hoist_cols(hoist);
+  std::vector<std::string> names = {tile_name(plan, hc > 0)};
   if (has_stream(plan)) names.push_back(stream_name(plan));
   std::vector<char> cubin;
   std::vector<std::string> lowered;
@@ -619,7 +793,8 @@ Module* module_for(const HostPlan& plan) {
     } else {
       const int tile_smem = kMaxCols * kJitTile * static_cast<int>(sizeof(double));
       drv.set_attribute(m.tile, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, tile_smem);
-      drv.occupancy(&m.tile_occ, m.tile, kJitThreads, plan.dev.ncols * kJitTile * sizeof(double));
+      m.smem_cols = plan.dev.ncols + hc;
+      drv.occupancy(&m.tile_occ, m.tile, kJitThreads, m.smem_cols * kJitTile * sizeof(double));
       if (m.tile_occ < 1) m.tile_occ = 1;
       if (m.stream) {
         const int ss = kJitStages * kJitTile * static_cast<int>(sizeof(double));
@@ -639,18 +814,29 @@ Module* module_for(const HostPlan& plan) {
 
 bool jit_prepare(const HostPlan& plan) {
   if (!jit_enabled() || plan.programs.empty()) return false;
-  return module_for(plan) != nullptr;
+  return module_for(plan, nullptr) != nullptr;
 }
 
 NllLaunchInfo launch_nll_jit(const HostPlan& plan, const ColPtrs& cols, long long n, const double* d_consts, int P,
                              void* scratch, SumPair* d_out, unsigned long long* d_bad, cudaStream_t stream,
-                             cudaEvent_t ev_start, cudaEvent_t ev_stop) {
+                             const double* h_rows, cudaEvent_t ev_start, cudaEvent_t ev_stop) {
   NllLaunchInfo info;
   if (P <= 0) return info;
-  Module* m = module_for(plan);
-  if (!m) usage_error("internal: launch_nll_jit without a module");
   DriverApi& drv = driver();
   const int sms = device_sm_count();
+  bool aligned = true;
+  for (int c = 0; c < plan.dev.ncols; ++c) aligned = aligned && (reinterpret_cast<uintptr_t>(cols.c[c]) & 15) == 0;
+  const bool streaming = has_stream(plan) && P <= kJitStreamMaxP && aligned && std::getenv("FFB_NO_STREAM") == nullptr;
+  // launch-constant formula subtrees (tile kernel only): cached per staged tile
+  ExprHoist hoist;
+  if (!streaming && std::getenv("FFB_NO_CONST_CACHE") == nullptr) hoist = analyse_expr_hoist(plan, h_rows, P);
+  const ExprHoist* hp = hoist.slots.empty() ? nullptr : &hoist;
+  Module* m = module_for(plan, hp);
+  if (!m && hp) {  // the cached build failed to compile: the plain formula build
+    hp = nullptr;
+    m = module_for(plan, nullptr);
+  }
+  if (!m) usage_error("internal: launch_nll_jit without a module");
   DevPlan dp = plan.dev;
   ColPtrs cp = cols;
   long long nn = n;
@@ -660,11 +846,9 @@ NllLaunchInfo launch_nll_jit(const HostPlan& plan, const ColPtrs& cols, long lon
   unsigned long long* bad = d_bad;
   cudaMemsetAsync(d_bad, 0xff, sizeof(unsigned long long) * P, stream);
   const long long ntl = (n + kJitTile - 1) / kJitTile;
-  bool aligned = true;
-  for (int c = 0; c < plan.dev.ncols; ++c) aligned = aligned && (reinterpret_cast<uintptr_t>(cols.c[c]) & 15) == 0;
   CUresult rc;
   int rows;
-  if (m->stream && P <= kJitStreamMaxP && aligned && std::getenv("FFB_NO_STREAM") == nullptr) {
+  if (m->stream && streaming) {
     long long G = static_cast<long long>(sms) * m->stream_occ;
     if (G > ntl) G = ntl;
     int ntiles = static_cast<int>(ntl);
@@ -679,7 +863,7 @@ NllLaunchInfo launch_nll_jit(const HostPlan& plan, const ColPtrs& cols, long lon
   } else {
     int ntiles = static_cast<int>(ntl < 1 ? 1 : ntl);
     const long long slots = static_cast<long long>(sms) * m->tile_occ;
-    long long want = (8 * slots + ntiles - 1) / ntiles;
+    long long want = (nll_waves() * slots + ntiles - 1) / ntiles;
     if (want < 1) want = 1;
     if (want > P) want = P;
     int pchunk = static_cast<int>((P + want - 1) / want);
@@ -687,11 +871,12 @@ NllLaunchInfo launch_nll_jit(const HostPlan& plan, const ColPtrs& cols, long lon
     void* args[] = {&dp, &cp, &nn, &kc, &PP, &pchunk, &ntiles, &partial, &bad};
     if (ev_start) cudaEventRecord(ev_start, stream);
     rc = drv.launch(m->tile, static_cast<unsigned>(static_cast<long long>(ntiles) * nchunks), 1, 1, kJitThreads, 1, 1,
-                    plan.dev.ncols * kJitTile * sizeof(double), reinterpret_cast<CUstream>(stream), args, nullptr);
+                    m->smem_cols * kJitTile * sizeof(double), reinterpret_cast<CUstream>(stream), args, nullptr);
     if (ev_stop) cudaEventRecord(ev_stop, stream);
     rows = ntiles;
     info.nchunks = nchunks;
     info.grid = ntiles * nchunks;
+    info.cached = hoist_cols(hp);
   }
   if (rc != CUDA_SUCCESS) numeric_error("cuLaunchKernel (formula-specialised likelihood) failed: " + std::to_string(rc));
   launch_reduce(partial, rows, P, d_out, stream);
@@ -774,14 +959,9 @@ PlanModule* plan_module(const DevPlan& d, int ks) {
 
 }  // namespace
 
-std::string plan_spec_source(const DevPlan& d) {
+std::string plan_spec_struct(const DevPlan& d) {
   std::ostringstream o;
-  // FFB_CONST_BANK: the exp / log polynomial constants as constant-bank DFMA operands
-  // instead of 64-bit immediates materialised per use (A/B, profiles/r01_ab1: +0.2-2.3 %
-  // on C2-C4, -0.5 % on C1)
-  o << "// generated by jit.cpp: the launch's term list for nll_kernel<..., PlanSpec>\n"
-       "#define FFB_CONST_BANK 1\n"
-       "#include \"plan.hpp\"\nnamespace ffb {\nstruct PlanSpec {\n"
+  o << "#include \"plan.hpp\"\nnamespace ffb {\nstruct PlanSpec {\n"
        "  static constexpr bool kOn = true;\n"
     << "  static constexpr int nterms = " << d.nterms << ";\n"
     << "  static constexpr bool simple = " << (d.simple ? "true" : "false") << ";\n"
@@ -791,8 +971,17 @@ std::string plan_spec_source(const DevPlan& d) {
     o << (i ? ", " : "") << "{" << t.kind << ", " << t.col << ", " << t.order << ", " << t.flags << ", " << t.coff
       << "}";
   }
-  o << "};\n};\n}  // namespace ffb\n#include \"kernels_device.cuh\"\n";
+  o << "};\n};\n}  // namespace ffb\n";
   return o.str();
+}
+
+std::string plan_spec_source(const DevPlan& d) {
+  // FFB_CONST_BANK: the exp / log polynomial constants as constant-bank DFMA operands
+  // instead of 64-bit immediates materialised per use (A/B, profiles/r01_ab1: +0.2-2.3 %
+  // on C2-C4, -0.5 % on C1)
+  return "// generated by jit.cpp: the launch's term list for nll_kernel<..., PlanSpec>\n"
+         "#define FFB_CONST_BANK 1\n" +
+         plan_spec_struct(d) + "#include \"kernels_device.cuh\"\n";
 }
 
 namespace {

@@ -14,14 +14,36 @@
 #include <cuda_runtime.h>
 
 #include <string>
+#include <vector>
 
 #include "kernels.cuh"
 #include "plan_build.hpp"
 
 namespace ffb {
 
-// The generated formula functions for `plan` (prepended to kernels_device.cuh).
-std::string jit_expression_source(const HostPlan& plan);
+// Launch-constant formula subtrees: a maximal subtree of an Expression term whose only
+// inputs are x, constants and parameters bitwise identical over every point of the
+// launch is computed once per staged tile into a shared-memory column (the tile kernel's
+// launch-constant builds) and read by every point; values bit-identical to the
+// uncached formula.  ArgusBG spelled as the reference's formula, m0 fixed:
+// x*sqrt(1-(x/m0)^2) and 1-(x/m0)^2 are cached, each point computes exp(c*t) and a product.
+struct HoistSlot {
+  int term;        // plan term
+  int prog;        // program offset (DevPlan::prog)
+  int begin, end;  // instruction range of the subtree (inclusive), absolute indices
+  int col;         // shared-memory column of the cached value
+  int xcol;        // the term's data column
+  int coff;        // the term's constant-row offset
+};
+struct ExprHoist {
+  std::vector<HoistSlot> slots;
+};
+// The cacheable subtrees of a launch of P points (host constant rows `rows`, P x stride).
+ExprHoist analyse_expr_hoist(const HostPlan& plan, const double* rows, int P);
+
+// The generated formula functions for `plan` (prepended to kernels_device.cuh), with
+// the cached-subtree variants when `hoist` lists any.
+std::string jit_expression_source(const HostPlan& plan, const ExprHoist* hoist = nullptr);
 
 // Whether the JIT path is switched on (default: on; FFB_NO_EXPR_JIT=1 or
 // ffcu_expression_jit(0) turns it off).
@@ -34,9 +56,10 @@ bool jit_prepare(const HostPlan& plan);
 std::string jit_status();
 
 // As launch_nll, through the plan's formula-specialised kernels (jit_prepare first).
+// h_rows: the launch's host constant rows (P x stride), for the launch-constant subtrees.
 NllLaunchInfo launch_nll_jit(const HostPlan& plan, const ColPtrs& cols, long long n, const double* d_consts, int P,
                              void* scratch, SumPair* d_out, unsigned long long* d_bad, cudaStream_t stream,
-                             cudaEvent_t ev_start = nullptr, cudaEvent_t ev_stop = nullptr);
+                             const double* h_rows, cudaEvent_t ev_start = nullptr, cudaEvent_t ev_stop = nullptr);
 
 // Plan-specialised gradient pass (kernels_device.cuh nll_grad_spec_kernel): one point,
 // single-column single-sum plans without Expression leaves, aligned column.
@@ -69,6 +92,6 @@ NllLaunchInfo launch_nll_spec(const DevPlan& launch, const ColPtrs& cols, long l
 // Compiles the plan's kernels (the generated formulas + kernels_device.cuh, both kernel
 // instantiations) to sm_100a SASS without loading them: the CPU-side check of the
 // generated code (NVRTC needs no GPU).
-bool jit_compile_only(const HostPlan& plan, std::string* log);
+bool jit_compile_only(const HostPlan& plan, std::string* log, const ExprHoist* hoist = nullptr);
 
 }  // namespace ffb

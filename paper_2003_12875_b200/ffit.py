@@ -550,11 +550,17 @@ def expression_jit_status() -> str:
     return lib().ffcu_expression_jit_status().decode()
 
 
-def expression_jit_source(model: Model, compile: bool = False) -> str:
+def expression_jit_source(model: Model, compile: bool = False, points=None) -> str:
     """The generated straight-line formula code of a model (compile=True also NVRTC-compiles
-    the kernels around it; host only)."""
+    the kernels around it; host only).  With `points` (P x n_params): the code of a launch
+    over them, launch-constant formula subtrees cached per tile."""
     buf = ctypes.create_string_buffer(1 << 20)
-    _check(lib().ffcu_expression_jit_source(model.handle, 1 if compile else 0, buf, 1 << 20))
+    if points is None:
+        _check(lib().ffcu_expression_jit_source(model.handle, 1 if compile else 0, buf, 1 << 20))
+    else:
+        pts = _f64(np.atleast_2d(points))
+        _check(lib().ffcu_expression_jit_source_points(model.handle, _dp(pts), pts.shape[0], 1 if compile else 0,
+                                                       buf, 1 << 20))
     return buf.value.decode()
 
 

@@ -114,3 +114,18 @@ def test_formula_source_mirrors_the_program():
                              "pdf e Expression(\"1 + a*x^3 - x^2/4 + pow(x, 2.5)\", x, a)\n")
     src = fb.expression_jit_source(m)
     assert src.count("__dmul_rn") >= 4 and "ffb_pow" in src and "k[2]" in src
+
+
+def test_formula_launch_constant_subtrees_compile_with_nvrtc():
+    """With m0 fixed over a launch's points, the reference's Argus formula's m0-only subtrees
+    (x*sqrt(1-(x/m0)^2), 1-(x/m0)^2) move to the per-tile cache; the source compiles."""
+    from paper_2003_12875_b200 import configs
+    w = configs.C2
+    m = fb.Model.from_string(configs.REFERENCE_TEXTS[w.name])
+    mo = fb.Model.from_string(w.text)
+    by = [dict(zip(mo.param_names, r)) for r in w.points(mo, n_points=12)]
+    pts = np.array([[d[n] for n in m.param_names] for d in by])
+    src = fb.expression_jit_source(m, compile=True, points=pts)
+    assert "FFB_EXPR_HOIST" in src and src.count("// column ") == 2
+    pts[3, m.param_names.index("m0")] += 1e-4  # m0 no longer launch-constant: nothing cached
+    assert "FFB_EXPR_HOIST" not in fb.expression_jit_source(m, points=pts)

@@ -623,6 +623,38 @@ def test_expression_jit_matches_interpreter(name):
     assert np.all(np.abs(many_j - many_i) <= 1e-13 * np.abs(many_i))
 
 
+def test_expression_launch_constant_subtrees_bit_identical():
+    """The reference's config-2 text (ArgusBG as a formula): with m0 fixed over the launch,
+    x*sqrt(1-(x/m0)^2) and 1-(x/m0)^2 are computed once per staged tile; one more point with
+    another m0 leaves no launch-constant subtree, and the launch runs the plain formula
+    build.  The shared points' values are bitwise equal either way and match the oracle on
+    the native spelling."""
+    w = configs.C2
+    text = configs.REFERENCE_TEXTS[w.name]
+    m = fb.Model.from_string(text)
+    mo = fb.Model.from_string(w.text)
+    cols, _ = fb.sample_host(mo, 120_013, 31)
+    ds = fb.DataSet.from_columns(cols)
+    by = [dict(zip(mo.param_names, r)) for r in w.points(mo, n_points=16)]
+    pts = np.array([[d[n] for n in m.param_names] for d in by])
+    was = fb.expression_jit(True)
+    try:
+        cached, bad, _ = fb.nll_points(m, ds, pts)
+        assert fb.last_launch_jit(m) == 1 and fb.last_launch_cached(m) == 2, fb.expression_jit_status()
+        other = pts[:1].copy()
+        other[0, m.param_names.index("m0")] *= 1 + 1e-4
+        plain, _, _ = fb.nll_points(m, ds, np.vstack([pts, other]))
+        assert fb.last_launch_cached(m) == 0
+    finally:
+        fb.expression_jit(was)
+    assert np.array_equal(cached, plain[:16])
+    o = OracleModel(w.text)
+    for p in (0, 15):
+        _, comp, ob = o.nll([cols["x"]], np.array([by[p][n] for n in mo.param_names]))
+        assert bad[p] == ob == -1
+        assert abs(cached[p] - comp) <= NLL_TOL * abs(comp)
+
+
 # ------------------------------------------------------------------ plan-specialised builds
 
 def _spec_cases():
