@@ -378,7 +378,7 @@ ExprHoist analyse_expr_hoist(const HostPlan& plan, const double* rows, int P) {
   ExprHoist out;
   if (!rows || P < 2) return out;
   const DevPlan& d = plan.dev;
-  int next_col = d.ncols + 2 * d.nderived;
+  int next_col = d.ncols + d.ncached;
   auto bits = [](double v) {
     unsigned long long b;
     std::memcpy(&b, &v, sizeof b);
@@ -939,7 +939,7 @@ PlanModule* plan_module(const DevPlan& d, int ks) {
         (names.size() < 2 || drv.get_function(&m.stream, m.mod, lowered[1].c_str()) == CUDA_SUCCESS)) {
       drv.set_attribute(m.fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
                         kMaxCols * kJitTile * static_cast<int>(sizeof(double)));
-      drv.occupancy(&m.occ, m.fn, kJitThreads, (d.ncols + 2 * d.nderived) * kJitTile * sizeof(double));
+      drv.occupancy(&m.occ, m.fn, kJitThreads, (d.ncols + d.ncached) * kJitTile * sizeof(double));
       if (m.occ < 1) m.occ = 1;
       if (m.stream) {
         const int ss = kJitStages * kJitTile * static_cast<int>(sizeof(double));
@@ -971,6 +971,13 @@ std::string plan_spec_struct(const DevPlan& d) {
     o << (i ? ", " : "") << "{" << t.kind << ", " << t.col << ", " << t.order << ", " << t.flags << ", " << t.coff
       << "}";
   }
+  o << "};\n  static constexpr int nderived = " << d.nderived << ";\n  static constexpr DevDerive dv["
+    << (d.nderived > 0 ? d.nderived : 1) << "] = {";
+  for (int i = 0; i < d.nderived; ++i) {
+    const DevDerive& v = d.dv[i];
+    o << (i ? ", " : "") << "{" << v.col << ", " << v.coff << ", " << v.kind << ", " << v.order << ", " << v.dst << "}";
+  }
+  if (d.nderived == 0) o << "{0, 0, 0, 0, 0}";
   o << "};\n};\n}  // namespace ffb\n";
   return o.str();
 }
@@ -1069,7 +1076,7 @@ NllLaunchInfo launch_nll_spec(const DevPlan& launch, const ColPtrs& cols, long l
   if (ev_start) cudaEventRecord(ev_start, stream);
   const CUresult rc =
       drv.launch(m->fn, static_cast<unsigned>(static_cast<long long>(ntiles) * nchunks), 1, 1, kJitThreads, 1, 1,
-                 (launch.ncols + 2 * launch.nderived) * kJitTile * sizeof(double),
+                 (launch.ncols + launch.ncached) * kJitTile * sizeof(double),
                  reinterpret_cast<CUstream>(stream), args, nullptr);
   if (ev_stop) cudaEventRecord(ev_stop, stream);
   if (rc != CUDA_SUCCESS) numeric_error("cuLaunchKernel (plan-specialised likelihood) failed: " + std::to_string(rc));

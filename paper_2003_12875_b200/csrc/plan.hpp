@@ -41,6 +41,9 @@ enum LeafKind : int {
   LK_ARGUS_CACHED = 8,  // c: as LK_ARGUS; order = shared-memory column of the tile's cached
                         // (t, x sqrt t) pair (DevPlan::dv): ArgusBG with m0 and p = 1/2 the same
                         // for every point of the launch (a launch-constant branch)
+  LK_LEAF_CACHED = 9,   // c: as the original leaf (only coef is read); order = shared-memory
+                        // column of the tile's cached leaf values: every shape parameter of
+                        // the leaf the same for every point of the launch (a yield-only fit)
 };
 
 // Expression programs (expr.hpp): postfix instructions, END-terminated on the device.
@@ -101,14 +104,19 @@ struct SumPair {
 constexpr unsigned long long kNoInvalid = ~0ull;
 
 // Launch-constant branch cache (RooFit's constant-term optimisation, restated per
-// launch): an ArgusBG term whose m0 and p = 1/2 are identical for every point of the
-// launch has a data-only part t = 1 - (x/m0)^2, u = x sqrt(t) (both 0 for t <= 0) that
-// the tile kernel computes ONCE per staged tile into two extra shared-memory columns;
-// each point then evaluates u * exp(c t) (cache_launch_constants, kernels.cu).
-constexpr int kMaxDerived = 2;
+// launch): a leaf whose shape parameters are all identical for every point of the launch
+// (only its coefficient -- fraction, yield, normalisation -- varies) is evaluated ONCE per
+// staged tile into an extra shared-memory column; an ArgusBG term whose m0 and p = 1/2 are
+// identical has a data-only part t = 1 - (x/m0)^2, u = x sqrt(t) (both 0 for t <= 0)
+// computed once per tile into two columns, each point then evaluates u * exp(c t)
+// (cache_launch_constants, kernels.cu).
+constexpr int kMaxDerived = 8;
 struct DevDerive {
   int col;   // source data column
-  int coff;  // the term's offset in a point's constant row (m0 = [1], 1/m0 = [4])
+  int coff;  // the term's offset in a point's constant row (ArgusBG pair: m0 = [1], 1/m0 = [4])
+  int kind;  // LK_ARGUS_CACHED: the ArgusBG (t, u) pair; else the cached leaf's kind
+  int order; // the cached leaf's order (Chebychev / Polynomial)
+  int dst;   // first shared-memory column written
 };
 
 struct DevPlan {
@@ -118,7 +126,8 @@ struct DevPlan {
   int simple;  // 1: a single sum of terms (no product structure)
   DevTerm t[kMaxTerms];
   const ExprInstr* prog;  // device copy of the plan's Expression programs (or null)
-  int nderived = 0;       // launch-constant caches (tile kernel only); 2 smem columns each
+  int nderived = 0;       // launch-constant caches (tile kernel only)
+  int ncached = 0;        // shared-memory columns they fill (after the ncols data columns)
   DevDerive dv[kMaxDerived] = {};
 };
 

@@ -159,6 +159,41 @@ pdf bkg ArgusBG(x, m0, c, p)
         assert ba[p] == ob == -1 and abs(va[p] - comp) <= NLL_TOL * abs(comp)
 
 
+@pytest.mark.parametrize("name", ["c4_yields_only", "c3_cheb_fixed"])
+def test_launch_constant_whole_leaves(name):
+    """Leaves whose shape parameters are all fixed over a launch (a yield-only fit of the
+    config-4 mixture; config 3 with the Chebychev coefficients fixed) are evaluated once per
+    staged tile; each point reads them back.  Bitwise equal to the uncached launch (one more
+    point that moves every shape parameter) and to the oracle."""
+    w = configs.C4 if name.startswith("c4") else configs.C3
+    m, ds, cols, o = setup(w.text, 60_007, 41)
+    base = m.theta()
+    names = m.param_names
+    if name.startswith("c4"):
+        vary = [k for k, n in enumerate(names) if n.startswith("n")]   # yields only
+        expect = 6
+    else:
+        vary = [k for k, n in enumerate(names) if not n.startswith("a")]  # everything but a1..a3
+        expect = 1
+    pts = np.tile(base, (12, 1))
+    for p in range(12):
+        for k in vary:
+            pts[p, k] = base[k] * (1.0 + 1e-3 * (p - 6)) if base[k] != 0 else 1e-3 * (p - 6)
+    cached, bad, _ = fb.nll_points(m, ds, pts)
+    assert fb.last_launch_cached(m) == expect
+    other = pts[:1].copy()
+    for k in range(len(names)):
+        if k not in vary and not m.is_constant(names[k]):
+            other[0, k] = base[k] * (1 + 1e-4) if base[k] != 0 else 1e-4
+    plain, _, _ = fb.nll_points(m, ds, np.vstack([pts, other]))
+    assert fb.last_launch_cached(m) == 0
+    assert np.array_equal(cached, plain[:12])
+    for p in (0, 11):
+        _, comp, ob = o.nll(cols, pts[p])
+        assert bad[p] == ob == -1
+        assert abs(cached[p] - comp) <= NLL_TOL * abs(comp)  # the oracle includes the extended term
+
+
 def test_more_than_512_points_split_launches():
     w = configs.C1
     m, ds, cols, o = setup(w.text, 20_000, 3)
