@@ -731,3 +731,33 @@ def test_plan_specialised_build_matches_static_build(name):
         _, comp, ob = o.nll(cols, pts[p])
         assert bad[p] == ob
         assert abs(spec[p] - comp) <= NLL_TOL * abs(comp)
+
+
+@pytest.mark.parametrize("name", list(_spec_cases()))
+def test_launch_constant_cache_every_leaf_kind(name):
+    """Only one free parameter moves over the launch's points, so every leaf that does not
+    read it is evaluated once per staged tile (the whole-leaf cache; every leaf kind and
+    plan shape of the gradient-test models).  Bitwise equal to the same points in a launch
+    where one more point moves every parameter (nothing cached), and to the oracle."""
+    from tests.test_gpu_grad import setup as grad_setup
+    text, n = _spec_cases()[name]
+    m, ds, cols = grad_setup(text, n, 202)
+    o = OracleModel(text)
+    base = m.theta()
+    free = [k for k, nm in enumerate(m.param_names) if not m.is_constant(nm)]
+    j = free[-1]
+    pts = np.tile(base, (12, 1))
+    for p in range(12):
+        pts[p, j] = base[j] * (1.0 + 2e-4 * (p - 6)) if base[j] != 0 else 1e-4 * (p - 6)
+    cached, bad, _ = fb.nll_points(m, ds, pts)
+    ncached = fb.last_launch_cached(m)
+    other = base.copy()
+    for k in range(len(base)):  # constant parameters too (ArgusBG's m0 in config 2)
+        other[k] = base[k] * (1 + 1e-4) if base[k] != 0 else 1e-4
+    plain, _, _ = fb.nll_points(m, ds, np.vstack([pts, other[None, :]]))
+    assert fb.last_launch_cached(m) == 0
+    assert np.array_equal(cached, plain[:12]), (ncached, np.max(np.abs(cached - plain[:12]) / np.abs(plain[:12])))
+    for p in (0, 11):
+        _, comp, ob = o.nll(cols, pts[p])
+        assert bad[p] == ob
+        assert abs(cached[p] - comp) <= NLL_TOL * abs(comp)
