@@ -443,10 +443,6 @@ ExprHoist analyse_expr_hoist(const HostPlan& plan, const double* rows, int P) {
   return out;
 }
 
-namespace {
-
-}  // namespace
-
 std::string jit_expression_source(const HostPlan& plan, const ExprHoist* hoist) {
   // Each formula becomes code over the thread's E events at once (one array per stack
   // depth, every operation an unrolled loop), so the compiler interleaves the events.
