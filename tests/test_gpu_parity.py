@@ -761,3 +761,44 @@ def test_launch_constant_cache_every_leaf_kind(name):
         _, comp, ob = o.nll(cols, pts[p])
         assert bad[p] == ob
         assert abs(cached[p] - comp) <= NLL_TOL * abs(comp)
+
+
+@pytest.mark.parametrize("n", [1, 2047, 2049, 10007])
+@pytest.mark.parametrize("shape", ["c4_yields_only", "c2_m0_fixed", "all_free"])
+def test_cached_and_specialised_paths_edge_cases(n, shape):
+    """The plan-specialised tile kernel with the launch-constant caches on ragged sizes,
+    non-finite events (first invalid index) and an 8-byte-aligned device view."""
+    w = configs.C4 if shape == "c4_yields_only" else configs.C2
+    m = fb.Model.from_string(w.text)
+    o = OracleModel(w.text)
+    cols, _ = fb.sample_host(m, n + 1, 61)
+    x = cols["x"]
+    base = m.theta()
+    names = m.param_names
+    pts = np.tile(base, (12, 1))
+    for p in range(12):
+        for k, name in enumerate(names):
+            moves = (name.startswith("n") if shape == "c4_yields_only"
+                     else not m.is_constant(name))
+            if moves:
+                pts[p, k] = base[k] * (1.0 + 2e-4 * (p - 6))
+    old = fb.plan_spec_min_work(0)
+    try:
+        for bad in (None, np.nan, np.inf):
+            y = x.copy()
+            if bad is not None and n > 3:
+                y[n // 2] = bad
+            full = fb.DataSet.from_columns({"x": y})
+            view = full.slice(1, n + 1)  # starts 8 bytes into the column: cooperative staging
+            for ds, xs in ((full, y), (view, y[1:n + 1])):
+                vals, fi, _ = fb.nll_points(m, ds, pts)
+                assert fb.last_launch_jit(m) == 2
+                for p in (0, 11):
+                    _, comp, ob = o.nll([xs], pts[p])
+                    assert fi[p] == ob
+                    if ob >= 0:
+                        assert math.isinf(vals[p])
+                    else:
+                        assert abs(vals[p] - comp) <= NLL_TOL * abs(comp)
+    finally:
+        fb.plan_spec_min_work(old)
