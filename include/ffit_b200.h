@@ -118,6 +118,10 @@ int ffcu_dataset_from_device(const char* const* names, const double* const* dev_
                              long long n, int device, ffit_dataset** out);
 /* Refill an owned dataset from host columns of the same shape. */
 int ffcu_dataset_copy_from_host(ffit_dataset* ds, const double* const* cols);
+/* The same, asynchronous on `stream` (a cudaStream_t): with pinned host columns the copy
+ * overlaps other work (double-buffered input pipelines); the caller orders it against
+ * the launches that read the dataset (events) and keeps the host columns alive. */
+int ffcu_dataset_copy_from_host_async(ffit_dataset* ds, const double* const* cols, void* stream);
 /* Rows [begin, end) as a zero-copy view (event sharding). */
 int ffcu_dataset_slice(const ffit_dataset* ds, long long begin, long long end, ffit_dataset** out);
 int ffcu_dataset_ncols(const ffit_dataset* ds);

@@ -62,6 +62,7 @@ SIGNATURES = {
     "ffcu_dataset_from_host": (I, [ctypes.POINTER(CP), ctypes.POINTER(DP), I, LL, ctypes.POINTER(VP)]),
     "ffcu_dataset_from_device": (I, [ctypes.POINTER(CP), ctypes.POINTER(VP), I, LL, I, ctypes.POINTER(VP)]),
     "ffcu_dataset_copy_from_host": (I, [VP, ctypes.POINTER(DP)]),
+    "ffcu_dataset_copy_from_host_async": (I, [VP, ctypes.POINTER(DP), VP]),
     "ffcu_dataset_slice": (I, [VP, LL, LL, ctypes.POINTER(VP)]),
     "ffcu_dataset_ncols": (I, [VP]),
     "ffcu_dataset_column_name": (CP, [VP, I]),

@@ -873,6 +873,16 @@ FFB_API int ffcu_dataset_copy_from_host(ffit_dataset* ds, const double* const* c
   });
 }
 
+FFB_API int ffcu_dataset_copy_from_host_async(ffit_dataset* ds, const double* const* cols, void* stream) {
+  return guarded([&] {
+    require(ds, "dataset");
+    require(cols, "cols");
+    if (!ds->d->owns) ffb::usage_error("cannot refill a view");
+    std::vector<const double*> c(cols, cols + ds->d->cols.size());
+    ds->d->copy_from_host_async(c, static_cast<cudaStream_t>(stream));
+  });
+}
+
 FFB_API int ffcu_dataset_slice(const ffit_dataset* ds, long long begin, long long end, ffit_dataset** out) {
   return guarded([&] {
     require(ds, "dataset");

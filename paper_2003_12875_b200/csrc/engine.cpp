@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -148,6 +149,18 @@ void DeviceDataset::copy_from_host(const std::vector<const double*>& host_cols) 
   }
 }
 
+void DeviceDataset::copy_from_host_async(const std::vector<const double*>& host_cols, cudaStream_t stream) {
+  if (host_cols.size() != cols.size()) usage_error("dataset: column count mismatch");
+  if (n == 0) return;
+  DeviceGuard g(device);
+  for (std::size_t i = 0; i < cols.size(); ++i) {
+    if (!host_cols[i]) usage_error("dataset: null host column");
+    cuda_check(cudaMemcpyAsync(cols[i], host_cols[i], static_cast<std::size_t>(n) * sizeof(double),
+                               cudaMemcpyHostToDevice, stream),
+               "cudaMemcpyAsync(H2D column)");
+  }
+}
+
 void DeviceDataset::download(int col, double* host_out) const {
   if (col < 0 || col >= static_cast<int>(cols.size())) usage_error("dataset: column index out of range");
   if (n == 0) return;
@@ -253,16 +266,21 @@ const double* Engine::upload_constants(const HostPlan& plan, const double* theta
   cuda_check(cudaEventSynchronize(staged_[k]), "cudaEventSynchronize");
   const int npar = static_cast<int>(m_.params.size());
   const int stride = plan.dev.stride;
-  // the points' constant rows are independent: spread them over the host pool when
-  // there are several (each row is validated; the first invalid point's error is raised)
+  // the points' constant rows are independent: spread them over the host pool when the
+  // rows are expensive (Simpson normalisations: Expression / ChiSquare / JohnsonSU), else
+  // build them here -- analytic rows take ~0.2-1 us, less than waking the pool (each row
+  // is validated; the first invalid point's error is raised)
   auto row = [&](int p) {
     build_constants(plan, m_, thetas + static_cast<std::size_t>(p) * npar,
                     h_consts_[k] + static_cast<std::size_t>(p) * stride, extra_scale);
   };
-  if (P >= 4) {
-    ThreadPool::instance().parallel_for(P, row);
+  const auto t0 = std::chrono::steady_clock::now();
+  row(0);
+  const double first_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+  if (P > 1 && first_us * (P - 1) > 100.0) {
+    ThreadPool::instance().parallel_for(P - 1, [&](int p) { row(p + 1); });
   } else {
-    for (int p = 0; p < P; ++p) row(p);
+    for (int p = 1; p < P; ++p) row(p);
   }
   cuda_check(cudaMemcpyAsync(d_consts_[k], h_consts_[k],
                              static_cast<std::size_t>(P) * stride * sizeof(double),

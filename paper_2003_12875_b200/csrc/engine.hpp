@@ -43,6 +43,7 @@ struct DeviceDataset {
                                              const std::vector<const double*>& dev_cols,
                                              long long n, int device);
   void copy_from_host(const std::vector<const double*>& host_cols);
+  void copy_from_host_async(const std::vector<const double*>& host_cols, cudaStream_t stream);
   void download(int col, double* host_out) const;
 };
 

@@ -244,6 +244,17 @@ class DataSet:
         cp = (DP * len(cols))(*[_dp(c) for c in cols])
         _check(lib().ffcu_dataset_copy_from_host(self._h, cp))
 
+    def copy_from_host_async(self, columns: dict, stream_ptr):
+        """Asynchronous refill on a CUDA stream (cudaStream_t as an int).  The columns must be
+        C-contiguous float64 arrays (pinned for a real overlap) that stay alive until the copy
+        has completed on that stream."""
+        cols = [columns[n] for n in self.names]
+        for c in cols:
+            if not (isinstance(c, np.ndarray) and c.dtype == np.float64 and c.flags.c_contiguous):
+                raise FfitError(1, "copy_from_host_async needs C-contiguous float64 columns")
+        cp = (DP * len(cols))(*[_dp(c) for c in cols])
+        _check(lib().ffcu_dataset_copy_from_host_async(self._h, cp, VP(stream_ptr)))
+
     def slice(self, begin, end) -> "DataSet":
         h = VP()
         _check(lib().ffcu_dataset_slice(self._h, begin, end, ctypes.byref(h)))
