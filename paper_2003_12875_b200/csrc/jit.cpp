@@ -898,11 +898,15 @@ struct PlanModule {
   int occ = 1, stream_occ = 1;
 };
 
-bool spec_has_stream(const DevPlan& d) { return d.ncols == 1 && d.simple && d.nderived == 0; }
+// the few-point streaming kernel: one column (any plan shape) or up to three (products
+// over several observables; kernels_device.cuh nll_stream_kernel NC > 1)
+constexpr int kSpecStreamMaxCols = 3;
+bool spec_has_stream(const DevPlan& d) { return d.ncols <= kSpecStreamMaxCols && d.nderived == 0; }
+int spec_stream_stages(const DevPlan& d) { return d.ncols == 1 ? kJitStages : 2; }
 
 std::string plan_spec_stream_name(const DevPlan& d, int ks) {
   return "&ffb::nll_stream_kernel<" + std::to_string(kJitThreads) + ", " + std::to_string(kJitE) + ", 2, " +
-         std::to_string(ks) + ", ffb::PlanSpec>";
+         std::to_string(ks) + ", ffb::PlanSpec, " + std::to_string(d.ncols) + ">";
 }
 std::map<std::tuple<int, std::string, int>, PlanModule> g_plan_mods;  // (device, source, mode)
 
@@ -938,7 +942,7 @@ PlanModule* plan_module(const DevPlan& d, int ks) {
       drv.occupancy(&m.occ, m.fn, kJitThreads, (d.ncols + d.ncached) * kJitTile * sizeof(double));
       if (m.occ < 1) m.occ = 1;
       if (m.stream) {
-        const int ss = kJitStages * kJitTile * static_cast<int>(sizeof(double));
+        const int ss = spec_stream_stages(d) * d.ncols * kJitTile * static_cast<int>(sizeof(double));
         drv.set_attribute(m.stream, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, ss);
         drv.occupancy(&m.stream_occ, m.stream, kJitThreads, ss);
         if (m.stream_occ < 1) m.stream_occ = 1;
@@ -1038,16 +1042,17 @@ NllLaunchInfo launch_nll_spec(const DevPlan& launch, const ColPtrs& cols, long l
   long long ntl = (n + kJitTile - 1) / kJitTile;
   if (ntl < 1) ntl = 1;
   int ntiles = static_cast<int>(ntl);
-  if (m->stream && P <= kJitStreamMaxP && (reinterpret_cast<uintptr_t>(cols.c[0]) & 15) == 0 &&
-      std::getenv("FFB_NO_STREAM") == nullptr) {
+  bool aligned = true;
+  for (int c = 0; c < launch.ncols; ++c) aligned = aligned && (reinterpret_cast<uintptr_t>(cols.c[c]) & 15) == 0;
+  if (m->stream && P <= kJitStreamMaxP && aligned && std::getenv("FFB_NO_STREAM") == nullptr) {
     // few points: the persistent streaming kernel (kernels_device.cuh nll_stream_kernel)
     long long G = static_cast<long long>(device_sm_count()) * m->stream_occ;
     if (G > ntl) G = ntl;
     void* sargs[] = {&dp, &cp, &nn, &kc, &PP, &ntiles, &partial, &bad};
     if (ev_start) cudaEventRecord(ev_start, stream);
     const CUresult rc = drv.launch(m->stream, static_cast<unsigned>(G), 1, 1, kJitThreads, 1, 1,
-                                   kJitStages * kJitTile * sizeof(double), reinterpret_cast<CUstream>(stream), sargs,
-                                   nullptr);
+                                   spec_stream_stages(launch) * launch.ncols * kJitTile * sizeof(double),
+                                   reinterpret_cast<CUstream>(stream), sargs, nullptr);
     if (ev_stop) cudaEventRecord(ev_stop, stream);
     if (rc != CUDA_SUCCESS) numeric_error("cuLaunchKernel (plan-specialised likelihood) failed: " + std::to_string(rc));
     launch_reduce(partial, static_cast<int>(G), P, d_out, stream);

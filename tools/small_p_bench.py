@@ -13,7 +13,7 @@ import paper_2003_12875_b200 as fb
 from paper_2003_12875_b200 import configs
 
 tag = "tile" if os.environ.get("FFB_NO_STREAM") else "stream"
-for w, n in ((configs.C1, 1_000_000), (configs.C2, 10_000_000), (configs.C5, 50_000_000)):
+for w, n in ((configs.C1, 1_000_000), (configs.C2, 10_000_000), (configs.C5, 50_000_000), (configs.C3, 50_000_000)):
     m = fb.Model.from_string(w.text)
     cols, _ = fb.sample_host(m, n, w.data_seed)
     ds = fb.DataSet.from_columns(cols)
