@@ -343,4 +343,71 @@ double ExprProgram::eval(const double* vars) const {
   return st[0];
 }
 
+double ExprProgram::eval_dual(const double* vars, const double* dvars, double* dvalue) const {
+  std::vector<double> st(max_depth > 0 ? max_depth : 1), sd(st.size());
+  int top = 0;
+  for (const ExprInstr& in : code) {
+    switch (in.op) {
+      case EX_CONST: st[top] = in.c; sd[top++] = 0.0; break;
+      case EX_VAR: st[top] = vars[in.slot]; sd[top++] = dvars[in.slot]; break;
+      case EX_ADD: --top; st[top - 1] += st[top]; sd[top - 1] += sd[top]; break;
+      case EX_SUB: --top; st[top - 1] -= st[top]; sd[top - 1] -= sd[top]; break;
+      case EX_MUL:
+        --top;
+        sd[top - 1] = sd[top - 1] * st[top] + st[top - 1] * sd[top];
+        st[top - 1] *= st[top];
+        break;
+      case EX_DIV: {
+        --top;
+        const double q = st[top - 1] / st[top];
+        sd[top - 1] = (sd[top - 1] - q * sd[top]) / st[top];
+        st[top - 1] = q;
+        break;
+      }
+      case EX_NEG: st[top - 1] = -st[top - 1]; sd[top - 1] = -sd[top - 1]; break;
+      case EX_POW: {  // a^b: b a^(b-1) da + a^b log(a) db
+        --top;
+        const double a = st[top - 1], b = st[top], r = expr_pow(a, b);
+        double d = sd[top - 1] == 0.0 ? 0.0 : b * expr_pow(a, b - 1.0) * sd[top - 1];
+        if (sd[top] != 0.0) d += r * std::log(a) * sd[top];
+        st[top - 1] = r;
+        sd[top - 1] = d;
+        break;
+      }
+      case EX_SQUARE: sd[top - 1] *= 2.0 * st[top - 1]; st[top - 1] *= st[top - 1]; break;
+      case EX_CUBE: {
+        const double v = st[top - 1];
+        sd[top - 1] *= 3.0 * v * v;
+        st[top - 1] = v * v * v;
+        break;
+      }
+      case EX_FOURTH: {
+        const double v = st[top - 1], v2 = v * v;
+        sd[top - 1] *= 4.0 * v2 * v;
+        st[top - 1] = v2 * v2;
+        break;
+      }
+      default: {
+        const double a = st[top - 1], r = apply_unary(in.op, a);
+        double g = 0.0;  // d op / d a
+        switch (in.op) {
+          case EX_EXP: g = r; break;
+          case EX_LOG: g = 1.0 / a; break;
+          case EX_SIN: g = std::cos(a); break;
+          case EX_COS: g = -std::sin(a); break;
+          case EX_SQRT: g = 0.5 / r; break;
+          case EX_ABS: g = a < 0.0 ? -1.0 : 1.0; break;
+          case EX_SINH: g = std::cosh(a); break;
+          default: g = 1.0 / std::sqrt(a * a + 1.0); break;  // asinh
+        }
+        st[top - 1] = r;
+        sd[top - 1] = sd[top - 1] == 0.0 ? 0.0 : g * sd[top - 1];
+        break;
+      }
+    }
+  }
+  *dvalue = sd[0];
+  return st[0];
+}
+
 }  // namespace ffb

@@ -36,6 +36,9 @@ struct ExprProgram {
 
   // Host evaluation with glibc math; `vars` holds nvars values.
   double eval(const double* vars) const;
+  // Forward-mode derivative: the value and d value / d t for variables moving as
+  // dvars * t (the analytic gradient's normalisation quadrature, model_grad.cpp).
+  double eval_dual(const double* vars, const double* dvars, double* dvalue) const;
 };
 
 // Parses and compiles `text` over the declared variable names.  Throws Usage with the

@@ -132,8 +132,16 @@ double Model::eval_unnorm_1d_grad(int id, const double* theta, double x, int j) 
     case Kind::ProdPdf:
       if (p.children.size() == 1) return eval_unnorm_1d_grad(p.children[0], theta, x, j);
       usage_error("eval_unnorm_1d_grad: multi-observable ProdPdf");
-    case Kind::Expression:
-      usage_error("Expression pdfs have no analytic derivative");
+    case Kind::Expression: {  // forward mode through the formula: every slot reading theta_j moves
+      std::vector<double> v(p.expr_vars.size()), dv(p.expr_vars.size());
+      for (std::size_t i = 0; i < p.expr_vars.size(); ++i) {
+        v[i] = p.expr_vars[i] < 0 ? x : theta[p.expr_vars[i]];
+        dv[i] = p.expr_vars[i] == j ? 1.0 : 0.0;
+      }
+      double d = 0.0;
+      p.program->eval_dual(v.data(), dv.data(), &d);
+      return d;
+    }
   }
   return 0.0;
 }

@@ -149,12 +149,16 @@ struct DevGradTerm {
   int pmask;    // leaf parameters differentiated on the device
   int factor;   // factor (sum) this term belongs to, 0..nfactors-1
   int fbeg, fend;  // factor range of the term's product
+  int seeds;    // Expression leaves: offset in DevGradPlan::seed of one slot mask per pmask bit
 };
 
 struct DevGradPlan {
   int nslots;
   int nfactors;
   DevGradTerm g[kMaxTerms];
+  // Expression leaves: per differentiated parameter, the formula variable slots reading it
+  // (bit s = constant-row entry 1 + s), the forward-mode seed of the device interpreter
+  int seed[kMaxGradSlots];
 };
 
 }  // namespace ffb

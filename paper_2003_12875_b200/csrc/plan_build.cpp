@@ -1,5 +1,6 @@
 #include "plan_build.hpp"
 
+#include <algorithm>
 #include <cmath>
 
 namespace ffb {
@@ -323,7 +324,7 @@ std::vector<double> coef_derivatives(const HostPlan& plan, const Model& m, const
 GradPlan compile_grad_plan(const HostPlan& plan, const Model& m) {
   GradPlan gp;
   const DevPlan& d = plan.dev;
-  int slot = 1;
+  int slot = 1, nseed = 0;
   gp.slot_param.assign(1, -1);
   int factor = 0, fbeg = 0;
   for (int i = 0; i < d.nterms; ++i) {
@@ -338,6 +339,18 @@ GradPlan compile_grad_plan(const HostPlan& plan, const Model& m) {
       gp.slot_param.push_back(leaf.params[k]);
       ++slot;
     }
+    if (d.t[i].kind == LK_EXPR) {  // one seed (variable-slot mask) per differentiated parameter
+      g.seeds = nseed;
+      for (std::size_t k = 0; k < leaf.params.size(); ++k) {
+        if (m.params[leaf.params[k]].constant) continue;
+        int mask = 0;
+        for (std::size_t s = 0; s < leaf.expr_vars.size(); ++s) {
+          if (leaf.expr_vars[s] == leaf.params[k]) mask |= 1 << s;
+        }
+        if (nseed < kMaxGradSlots) gp.dev.seed[nseed] = mask;
+        ++nseed;
+      }
+    }
     g.factor = factor;
     g.fbeg = fbeg;
     if (d.t[i].flags & TF_END_SUM) ++factor;
@@ -351,10 +364,15 @@ GradPlan compile_grad_plan(const HostPlan& plan, const Model& m) {
   }
   gp.dev.nslots = slot;
   gp.dev.nfactors = factor;
-  bool has_expr = false;
-  for (int i = 0; i < d.nterms; ++i) has_expr = has_expr || d.t[i].kind == LK_EXPR;
-  if (has_expr) {
-    gp.why = "Expression pdfs have no analytic derivative (use finite differences)";
+  int max_vars = 0;
+  for (int i = 0; i < d.nterms; ++i) {
+    if (d.t[i].kind == LK_EXPR) {
+      max_vars = std::max(max_vars, static_cast<int>(m.pdfs[plan.term_pdf[i]].expr_vars.size()));
+    }
+  }
+  if (nseed > kMaxGradSlots || max_vars > 30) {
+    gp.why = "Expression gradients: more than " + std::to_string(kMaxGradSlots) +
+             " differentiated formula parameters or 30 formula variables";
   } else if (slot > kMaxGradSlots) {
     gp.why = "gradient layout needs " + std::to_string(slot) + " accumulators; the device pass holds " +
              std::to_string(kMaxGradSlots);

