@@ -59,7 +59,8 @@ const char* ffit_last_error(void);
  * GPU path: ArgusBG(x, m0, c, p), Chebychev(x, a1..an), Polynomial(x, a1..an),
  * ProdPdf(p1, ..., pk) over distinct observables, AddPdf(c1, f1, ..., cn) (=
  * WeightedSum) and AddPdf(c1, y1, ..., cn, yn) (extended), several
- * `observable` lines.  Expression pdfs are rejected (no GPU kernel). */
+ * `observable` lines.  Expression("formula", vars...) pdfs run on the device
+ * (formula-specialised builds, else the device interpreter). */
 int ffit_model_load(const char* path, ffit_model** out);
 int ffit_model_parse(const char* text, ffit_model** out);
 void ffit_model_free(ffit_model* m);
