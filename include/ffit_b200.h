@@ -252,7 +252,9 @@ const char* ffcu_model_observable_name(const ffit_model* m, int i);
 int ffcu_fit_gradient(ffit_model* m, const ffit_dataset* ds, double tolerance,
                       long max_iterations, ffit_fit_result** out);
 /* analytic = 1: gradients from the fused NLL + gradient pass when the model's
- * layout fits it (ffcu_fit_gradient's default), 0: central finite differences. */
+ * layout fits it, 0: central finite differences, -1 (ffcu_fit_gradient's default):
+ * analytic except for models with Expression pdfs while their formula-specialised
+ * likelihood builds are on (2d+1 points of those beat the interpreter's gradient pass). */
 int ffcu_fit_gradient_opts(ffit_model* m, const ffit_dataset* ds, double tolerance,
                            long max_iterations, int analytic, ffit_fit_result** out);
 /* 1 if the fit's gradients came from the fused pass. */

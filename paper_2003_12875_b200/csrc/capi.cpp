@@ -941,7 +941,7 @@ FFB_API int ffit_fit(ffit_model* m, const ffit_dataset* ds, ffit_mode mode, doub
 
 FFB_API int ffcu_fit_gradient(ffit_model* m, const ffit_dataset* ds, double tolerance,
                               long max_iterations, ffit_fit_result** out) {
-  return ffcu_fit_gradient_opts(m, ds, tolerance, max_iterations, 1, out);
+  return ffcu_fit_gradient_opts(m, ds, tolerance, max_iterations, -1, out);
 }
 
 FFB_API int ffcu_fit_gradient_opts(ffit_model* m, const ffit_dataset* ds, double tolerance,
@@ -952,7 +952,15 @@ FFB_API int ffcu_fit_gradient_opts(ffit_model* m, const ffit_dataset* ds, double
     require(out, "out");
     ffb::FitOptions o;
     o.record_trace = true;
-    o.analytic_gradient = analytic != 0;
+    if (analytic < 0) {
+      // automatic: analytic gradients, except for models with Expression pdfs when their
+      // formula-specialised likelihood builds are on -- the gradient pass runs those
+      // formulas on the device interpreter, and 2d+1 points of the specialised build are
+      // faster (tools/expr_grad_bench.py: 0.9 vs 3.6 ms per gradient on the config-2 text)
+      o.analytic_gradient = engine(m).likelihood_plan().programs.empty() || !ffb::jit_enabled();
+    } else {
+      o.analytic_gradient = analytic != 0;
+    }
     if (tolerance > 0.0) o.tolerance = tolerance;
     if (max_iterations > 0) o.max_iterations = static_cast<int>(max_iterations);
     auto r = std::make_unique<ffit_fit_result>();

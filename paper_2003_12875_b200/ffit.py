@@ -451,13 +451,15 @@ def fit_to(model: Model, ds: DataSet, mode: EvalMode = EvalMode.Gpu, tolerance=0
     return _result(h)
 
 
-def fit_gradient(model: Model, ds: DataSet, tolerance=0.0, max_iterations=0, analytic=True) -> FitResult:
+def fit_gradient(model: Model, ds: DataSet, tolerance=0.0, max_iterations=0, analytic=None) -> FitResult:
     """Minuit-style BFGS.  analytic=True: gradients from the fused NLL + gradient pass
     (one point per iteration) when the model's layout fits it; False: central
-    differences, 2d+1 points per launch."""
+    differences, 2d+1 points per launch; None: automatic (analytic, except for models
+    with Expression pdfs whose formula-specialised builds make differences faster)."""
     h = VP()
-    _check(lib().ffcu_fit_gradient_opts(model.handle, ds.handle, tolerance, max_iterations,
-                                        1 if analytic else 0, ctypes.byref(h)))
+    flag = -1 if analytic is None else (1 if analytic else 0)
+    _check(lib().ffcu_fit_gradient_opts(model.handle, ds.handle, tolerance, max_iterations, flag,
+                                        ctypes.byref(h)))
     return _result(h)
 
 

@@ -619,17 +619,19 @@ def test_expression_sub_pdf_eval_batch_and_invalid_events():
     assert v.value == np.inf and v.first_invalid == 2
 
 
-def test_expression_fit_uses_analytic_gradients():
-    """A gradient fit of the reference's Argus-as-formula model runs on analytic gradients
-    (forward mode through the formula) and reaches the finite-difference fit's minimum."""
+def test_expression_fit_analytic_and_automatic():
+    """A gradient fit of the reference's Argus-as-formula model on analytic gradients
+    (forward mode through the formula) reaches the minimum of the automatic choice, which
+    for formula models is finite differences over the formula-specialised build."""
     text = EXPR_MODELS["argus_mix"][0]
     m = fb.Model.from_string(text)
     cols, _ = fb.sample_host(m, 20_000, 3)
     ds = fb.DataSet.from_columns(cols)
-    r = fb.fit_gradient(m, ds, tolerance=1e-10, max_iterations=200)
+    r = fb.fit_gradient(m, ds, tolerance=1e-10, max_iterations=200, analytic=True)
     assert r.converged and r.analytic_gradient
     m2 = fb.Model.from_string(text)
-    r2 = fb.fit_gradient(m2, ds, tolerance=1e-10, max_iterations=200, analytic=False)
+    # the automatic choice: finite differences over the formula-specialised build
+    r2 = fb.fit_gradient(m2, ds, tolerance=1e-10, max_iterations=200)
     assert r2.converged and not r2.analytic_gradient
     assert abs(r.nll_min - r2.nll_min) <= 1e-9 * abs(r2.nll_min)
     for a, b in zip(r.parameters, r2.parameters):
