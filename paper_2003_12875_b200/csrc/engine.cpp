@@ -10,6 +10,7 @@
 #include <cstring>
 #include <limits>
 #include <mutex>
+#include <sstream>
 #include <utility>
 
 namespace ffb {
@@ -180,6 +181,7 @@ Engine::~Engine() {
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(device_);
+    drop_graph();
     for (int k = 0; k < 2; ++k) {
       cudaFree(d_consts_[k]);
       cudaFreeHost(h_consts_[k]);
@@ -219,6 +221,7 @@ void Engine::ensure(int device, int P, std::size_t scratch) {
     }
   }
   if (P > cap_points_) {
+    drop_graph();  // the captured call reads the buffers replaced here
     const int cap = std::max(P, 16);
     for (int k = 0; k < 2; ++k) {
       cuda_check(cudaEventSynchronize(staged_[k]), "cudaEventSynchronize");
@@ -242,6 +245,7 @@ void Engine::ensure(int device, int P, std::size_t scratch) {
     cap_points_ = cap;
   }
   if (scratch > cap_scratch_) {
+    drop_graph();
     cuda_check(cudaStreamSynchronize(stream_), "cudaStreamSynchronize");
     cudaFree(d_scratch_);
     cuda_check(cudaMalloc(&d_scratch_, scratch), "cudaMalloc(scratch)");
@@ -308,41 +312,16 @@ int Engine::nll_points_device(const DeviceDataset& ds, const double* thetas, int
   }
   // the likelihood kernel evaluates p * 2^kPScaleLog2 (plan.hpp)
   const double* d_consts = upload_constants(plan_, thetas, P, s, std::ldexp(1.0, kPScaleLog2));
-  int launches = 0;
-  if (ds.n == 0) {
-    cuda_check(cudaMemsetAsync(d_pairs, 0, P * sizeof(SumPair), s), "cudaMemsetAsync");
-    cuda_check(cudaMemsetAsync(d_bad, 0xff, P * sizeof(unsigned long long), s), "cudaMemsetAsync");
-  } else {
-    ColPtrs cols;
-    bind_columns(plan_, ds, cols);
-    cudaEvent_t ea = nullptr, eb = nullptr;
-    {
-      std::lock_guard<std::mutex> lk(g_timer_mu);
-      if (g_timer_on) {
-        cuda_check(cudaEventCreate(&ea), "cudaEventCreate");
-        cuda_check(cudaEventCreate(&eb), "cudaEventCreate");
-        g_timer_events.emplace_back(ea, eb);
-      }
+  cudaEvent_t ea = nullptr, eb = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_timer_mu);
+    if (g_timer_on && ds.n > 0) {
+      cuda_check(cudaEventCreate(&ea), "cudaEventCreate");
+      cuda_check(cudaEventCreate(&eb), "cudaEventCreate");
+      g_timer_events.emplace_back(ea, eb);
     }
-    if (!plan_.programs.empty() && jit_prepare(plan_)) {
-      // Expression leaves: the formula-specialised build (jit.cpp) instead of the interpreter
-      last_ = launch_nll_jit(plan_, cols, ds.n, d_consts, P, d_scratch_, d_pairs, d_bad, s, h_consts_[slot_], ea, eb);
-    } else {
-      // launch-constant branches (ArgusBG with m0 fixed over the launch) cached per tile
-      DevPlan lp = plan_.dev;
-      const int cached = cache_launch_constants(lp, h_consts_[slot_], P);
-      const int ks = plan_kind_set(lp, h_consts_[slot_], P);
-      if (plan_spec_applies(plan_, lp, ds.n, P) && plan_spec_prepare(lp, ks)) {
-        // the tile kernel compiled around this launch's term list (jit.cpp; cached)
-        last_ = launch_nll_spec(lp, cols, ds.n, d_consts, P, d_scratch_, d_pairs, d_bad, s, ks, nll_waves(), ea, eb);
-      } else {
-        last_ = launch_nll(lp, cols, ds.n, d_consts, P, d_scratch_, d_pairs, d_bad, s, ks, ea, eb);
-      }
-      last_.cached = cached;
-    }
-    launches = last_.launches;
-    cuda_check(cudaGetLastError(), "launch_nll");
   }
+  const int launches = launch_device(ds, P, d_consts, h_consts_[slot_], d_pairs, d_bad, s, ea, eb);
   if (s != stream_) {
     cudaEvent_t ev;
     cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
@@ -354,7 +333,147 @@ int Engine::nll_points_device(const DeviceDataset& ds, const double* thetas, int
   return launches;
 }
 
+int Engine::launch_device(const DeviceDataset& ds, int P, const double* d_consts, const double* h_rows,
+                          SumPair* d_pairs, unsigned long long* d_bad, cudaStream_t s, cudaEvent_t ea,
+                          cudaEvent_t eb) {
+  if (ds.n == 0) {
+    cuda_check(cudaMemsetAsync(d_pairs, 0, P * sizeof(SumPair), s), "cudaMemsetAsync");
+    cuda_check(cudaMemsetAsync(d_bad, 0xff, P * sizeof(unsigned long long), s), "cudaMemsetAsync");
+    return 0;
+  }
+  ColPtrs cols;
+  bind_columns(plan_, ds, cols);
+  if (!plan_.programs.empty() && jit_prepare(plan_)) {
+    // Expression leaves: the formula-specialised build (jit.cpp) instead of the interpreter
+    last_ = launch_nll_jit(plan_, cols, ds.n, d_consts, P, d_scratch_, d_pairs, d_bad, s, h_rows, ea, eb);
+  } else {
+    // launch-constant branches (ArgusBG with m0 fixed over the launch) cached per tile
+    DevPlan lp = plan_.dev;
+    const int cached = cache_launch_constants(lp, h_rows, P);
+    const int ks = plan_kind_set(lp, h_rows, P);
+    if (plan_spec_applies(plan_, lp, ds.n, P) && plan_spec_prepare(lp, ks)) {
+      // the tile kernel compiled around this launch's term list (jit.cpp; cached)
+      last_ = launch_nll_spec(lp, cols, ds.n, d_consts, P, d_scratch_, d_pairs, d_bad, s, ks, nll_waves(), ea, eb);
+    } else {
+      last_ = launch_nll(lp, cols, ds.n, d_consts, P, d_scratch_, d_pairs, d_bad, s, ks, ea, eb);
+    }
+    last_.cached = cached;
+  }
+  cuda_check(cudaGetLastError(), "launch_nll");
+  return last_.launches;
+}
+
+// What launch_device would run for these rows: the key under which a captured graph of
+// the launch stays valid (the dataset's columns and size, P, and every launch decision).
+std::string Engine::launch_signature(const DeviceDataset& ds, int P, const double* h_rows) const {
+  std::ostringstream o;
+  o << ds.n << ':' << P;
+  for (const double* c : ds.cols) o << ':' << static_cast<const void*>(c);
+  if (!plan_.programs.empty()) {
+    const ExprHoist h = analyse_expr_hoist(plan_, h_rows, P);
+    o << "|jit" << jit_enabled();
+    for (const HoistSlot& v : h.slots) o << ',' << v.col << '/' << v.begin << '/' << v.end;
+  } else {
+    DevPlan lp = plan_.dev;
+    o << "|c" << cache_launch_constants(lp, h_rows, P) << "|k" << plan_kind_set(lp, h_rows, P) << "|s"
+      << plan_spec_applies(plan_, lp, ds.n, P);
+    for (int i = 0; i < lp.nterms; ++i) o << ',' << lp.t[i].kind << '/' << lp.t[i].order;
+  }
+  return o.str();
+}
+
+void Engine::drop_graph() {
+  if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+  graph_exec_ = nullptr;
+  graph_key_.clear();
+}
+
 NllResult Engine::nll_points(const DeviceDataset& ds, const double* thetas, int P) {
+  static const bool no_graphs = std::getenv("FFB_NO_GRAPHS") != nullptr;
+  bool timing;
+  {
+    std::lock_guard<std::mutex> lk(g_timer_mu);
+    timing = g_timer_on;
+  }
+  if (!no_graphs && !timing && P <= kGraphMaxPoints && ds.n > 0) return nll_points_graph(ds, thetas, P);
+  return nll_points_stream(ds, thetas, P);
+}
+
+// Few-point synchronous calls (a minimiser's function evaluations): the constant-row
+// upload, the launch sequence and the result read-back are one CUDA graph, captured on the
+// second call with the same launch signature and replayed while it holds -- one graph
+// launch instead of six API calls per evaluation.  The graph's H2D node reads the pinned
+// row buffer at execution, so each call only rewrites the rows.
+NllResult Engine::nll_points_graph(const DeviceDataset& ds, const double* thetas, int P) {
+  NllResult r;
+  r.value.resize(P);
+  r.pairs.resize(P);
+  r.first_invalid.resize(P);
+  const int npar = static_cast<int>(m_.params.size());
+  DeviceGuard g(ds.device);
+  ensure(ds.device, P, nll_scratch_bytes(ds.n, P, plan_.dev.ncols));
+  // rows into slot 0 (any earlier asynchronous copy out of it has completed)
+  cuda_check(cudaEventSynchronize(staged_[0]), "cudaEventSynchronize");
+  const int stride = plan_.dev.stride;
+  for (int p = 0; p < P; ++p) {
+    build_constants(plan_, m_, thetas + static_cast<std::size_t>(p) * npar,
+                    h_consts_[0] + static_cast<std::size_t>(p) * stride, std::ldexp(1.0, kPScaleLog2));
+  }
+  const std::string key = launch_signature(ds, P, h_consts_[0]);
+  const std::size_t bytes = static_cast<std::size_t>(P) * stride * sizeof(double);
+  auto sequence = [&] {
+    cuda_check(cudaMemcpyAsync(d_consts_[0], h_consts_[0], bytes, cudaMemcpyHostToDevice, stream_),
+               "cudaMemcpyAsync(consts)");
+    launch_device(ds, P, d_consts_[0], h_consts_[0], d_pairs_, d_bad_, stream_, nullptr, nullptr);
+    cuda_check(cudaMemcpyAsync(h_pairs_, d_pairs_, P * sizeof(SumPair), cudaMemcpyDeviceToHost, stream_),
+               "cudaMemcpyAsync(pairs)");
+    cuda_check(cudaMemcpyAsync(h_bad_, d_bad_, P * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream_),
+               "cudaMemcpyAsync(bad)");
+  };
+  int launches = 0;
+  if (graph_exec_ && key == graph_key_) {
+    cuda_check(cudaGraphLaunch(graph_exec_, stream_), "cudaGraphLaunch");
+    launches = graph_launches_;
+    last_ = graph_last_;
+  } else if (key == graph_key_) {  // second call with this signature: capture, then replay
+    cudaGraph_t graph = nullptr;
+    cuda_check(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+    try {
+      sequence();
+    } catch (...) {
+      cudaStreamEndCapture(stream_, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    cuda_check(cudaStreamEndCapture(stream_, &graph), "cudaStreamEndCapture");
+    const cudaError_t e = cudaGraphInstantiate(&graph_exec_, graph, 0);
+    cudaGraphDestroy(graph);
+    cuda_check(e, "cudaGraphInstantiate");
+    graph_launches_ = last_.launches;
+    graph_last_ = last_;
+    cuda_check(cudaGraphLaunch(graph_exec_, stream_), "cudaGraphLaunch");
+    launches = graph_launches_;
+  } else {  // a new signature: the plain sequence (it also compiles / loads any build)
+    drop_graph();
+    sequence();
+    graph_key_ = key;
+    launches = last_.launches;
+  }
+  cuda_check(cudaStreamSynchronize(stream_), "nll kernels");
+  count_launches(launches);
+  r.launches = launches;
+  for (int i = 0; i < P; ++i) {
+    r.pairs[i] = h_pairs_[i];
+    const bool bad = h_bad_[i] != kNoInvalid;
+    r.first_invalid[i] = bad ? static_cast<long long>(h_bad_[i]) : -1;
+    r.value[i] = bad ? std::numeric_limits<double>::infinity()
+                     : (h_pairs_[i].s + h_pairs_[i].c) +
+                           m_.extended_term(thetas + static_cast<std::size_t>(i) * npar, static_cast<double>(ds.n));
+  }
+  return r;
+}
+
+NllResult Engine::nll_points_stream(const DeviceDataset& ds, const double* thetas, int P) {
   NllResult r;
   r.value.resize(P);
   r.pairs.resize(P);

@@ -121,6 +121,13 @@ class Engine {
   cudaStream_t stream(int device);
 
  private:
+  static constexpr int kGraphMaxPoints = 8;  // few-point synchronous calls replay a CUDA graph
+  NllResult nll_points_graph(const DeviceDataset& ds, const double* thetas, int P);
+  NllResult nll_points_stream(const DeviceDataset& ds, const double* thetas, int P);
+  int launch_device(const DeviceDataset& ds, int P, const double* d_consts, const double* h_rows, SumPair* d_pairs,
+                    unsigned long long* d_bad, cudaStream_t s, cudaEvent_t ea, cudaEvent_t eb);
+  std::string launch_signature(const DeviceDataset& ds, int P, const double* h_rows) const;
+  void drop_graph();
   void bind_columns(const HostPlan& plan, const DeviceDataset& ds, ColPtrs& cols) const;
   void ensure(int device, int P, std::size_t scratch);
   const double* upload_constants(const HostPlan& plan, const double* thetas, int P, cudaStream_t s,
@@ -151,6 +158,10 @@ class Engine {
   SumPair* d_gslots_ = nullptr;
   SumPair* h_gslots_ = nullptr;  // pinned
   std::size_t cap_gslots_ = 0;
+  cudaGraphExec_t graph_exec_ = nullptr;  // the captured few-point call (nll_points_graph)
+  std::string graph_key_;
+  int graph_launches_ = 0;
+  NllLaunchInfo graph_last_{};
 };
 
 // Optional per-launch timing of the fused NLL kernel (CUDA events on the

@@ -836,3 +836,36 @@ def test_cached_and_specialised_paths_edge_cases(n, shape):
                         assert abs(vals[p] - comp) <= NLL_TOL * abs(comp)
     finally:
         fb.plan_spec_min_work(old)
+
+
+def test_few_point_calls_replay_a_cuda_graph():
+    """A minimiser's single-point calls: the first call with a launch signature runs the
+    plain sequence, the second captures it into a CUDA graph, later ones replay it (the
+    kernel timer disables graphs: the plain path).  Same bits on every path, and the
+    oracle's values at every point."""
+    w = configs.C2
+    m, ds, cols, o = setup(w.text, 100_003, 17)
+    pts = w.points(m, n_points=6)
+    fb.kernel_timer(True)
+    plain = [fb.nll_points(m, ds, pts[p:p + 1])[0][0] for p in range(6)]
+    fb.kernel_timer(False)
+    fb.kernel_timer_read()
+    launches0 = fb.kernel_launches()
+    graphed = [fb.nll_points(m, ds, pts[p:p + 1])[0][0] for p in range(6)]
+    again = [fb.nll_points(m, ds, pts[p:p + 1])[0][0] for p in range(6)]
+    assert fb.kernel_launches() - launches0 == 2 * 12  # replays still count their kernels
+    assert plain == graphed == again
+    for p in (0, 5):
+        _, comp, _ = o.nll(cols, pts[p])
+        assert abs(graphed[p] - comp) <= NLL_TOL * abs(comp)
+    # another dataset of the same size, then the first again: new signatures, same values
+    ds2 = fb.DataSet.from_columns({"x": cols[0].copy()})
+    v2 = [fb.nll_points(m, ds2, pts[:1])[0][0] for _ in range(3)]
+    v1 = [fb.nll_points(m, ds, pts[:1])[0][0] for _ in range(3)]
+    assert v2 == v1 == [plain[0]] * 3
+    # a point leaving ArgusBG's fast domain changes the kernel build (new signature)
+    bad = pts[:1].copy()
+    bad[0, m.param_names.index("c")] = -750.0
+    v3 = [fb.nll_points(m, ds, bad)[0][0] for _ in range(3)]
+    _, comp3, _ = o.nll(cols, bad[0])
+    assert v3[0] == v3[1] == v3[2] and abs(v3[0] - comp3) <= NLL_TOL * abs(comp3)

@@ -1,4 +1,4 @@
-"""Per-call latency of a single-point NLL (what a Minuit / Nelder-Mead caller pays per
+"""Per-call latency (FFB_NO_GRAPHS=1: without the CUDA-graph replay) of a single-point NLL (what a Minuit / Nelder-Mead caller pays per
 function evaluation) on small datasets: wall time per ffcu_nll_points call from Python,
 fused-kernel time, and the reference Nelder-Mead fit (ffit_fit) wall time per NLL call."""
 import os
@@ -21,13 +21,15 @@ for n in (10_000, 100_000, 1_000_000):
     for _ in range(20):
         fb.nll_points(m, ds, th)
     torch.cuda.synchronize()
-    fb.kernel_timer(True)
-    fb.kernel_timer_read()
     K = 200
     t0 = time.perf_counter()
-    for _ in range(K):
+    for _ in range(K):  # (no kernel timer here: it turns the CUDA-graph replay off)
         fb.nll_points(m, ds, th)
     wall = (time.perf_counter() - t0) / K
+    fb.kernel_timer(True)
+    fb.kernel_timer_read()
+    for _ in range(K):
+        fb.nll_points(m, ds, th)
     kms, c = fb.kernel_timer_read()
     fb.kernel_timer(False)
     start = w.points(m, n_points=1, seed=7)[0]
