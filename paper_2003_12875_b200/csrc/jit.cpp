@@ -912,9 +912,30 @@ std::map<std::tuple<int, std::string, int>, PlanModule> g_plan_mods;  // (device
 
 int spec_mode(const DevPlan& d, int ks) { return ks + (d.simple ? 0 : 3) + (d.nderived > 0 ? 6 : 0); }
 
+// the plan-specialised tile kernel's events per thread and minimum CTAs per SM
+// (FFB_SPEC_TILE="E,MINB" for A/B builds; nll_scratch_bytes sizes for E >= 4)
+struct SpecTile {
+  int e = kJitE, minb = 2;
+};
+const SpecTile& spec_tile() {
+  static const SpecTile t = [] {
+    SpecTile v;
+    if (const char* s = std::getenv("FFB_SPEC_TILE")) {
+      int e = 0, b = 0;
+      if (std::sscanf(s, "%d,%d", &e, &b) == 2 && (e == 4 || e == 8) && b >= 1 && b <= 4) {
+        v.e = e;
+        v.minb = b;
+      }
+    }
+    return v;
+  }();
+  return t;
+}
+
 std::string plan_spec_kernel_name(const DevPlan& d, int ks) {
-  return "&ffb::nll_kernel<" + std::to_string(kJitThreads) + ", " + std::to_string(kJitE) + ", " +
-         (d.ncols == 1 ? "true" : "false") + ", 2, " + std::to_string(spec_mode(d, ks)) + ", ffb::PlanSpec>";
+  return "&ffb::nll_kernel<" + std::to_string(kJitThreads) + ", " + std::to_string(spec_tile().e) + ", " +
+         (d.ncols == 1 ? "true" : "false") + ", " + std::to_string(spec_tile().minb) + ", " +
+         std::to_string(spec_mode(d, ks)) + ", ffb::PlanSpec>";
 }
 
 PlanModule* plan_module(const DevPlan& d, int ks) {
@@ -937,9 +958,10 @@ PlanModule* plan_module(const DevPlan& d, int ks) {
     if (drv.module_load(&m.mod, cubin.data()) == CUDA_SUCCESS &&
         drv.get_function(&m.fn, m.mod, lowered[0].c_str()) == CUDA_SUCCESS &&
         (names.size() < 2 || drv.get_function(&m.stream, m.mod, lowered[1].c_str()) == CUDA_SUCCESS)) {
+      const int st = kJitThreads * spec_tile().e;
       drv.set_attribute(m.fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
-                        kMaxCols * kJitTile * static_cast<int>(sizeof(double)));
-      drv.occupancy(&m.occ, m.fn, kJitThreads, (d.ncols + d.ncached) * kJitTile * sizeof(double));
+                        kMaxCols * st * static_cast<int>(sizeof(double)));
+      drv.occupancy(&m.occ, m.fn, kJitThreads, (d.ncols + d.ncached) * st * sizeof(double));
       if (m.occ < 1) m.occ = 1;
       if (m.stream) {
         const int ss = spec_stream_stages(d) * d.ncols * kJitTile * static_cast<int>(sizeof(double));
@@ -1067,6 +1089,10 @@ NllLaunchInfo launch_nll_spec(const DevPlan& launch, const ColPtrs& cols, long l
     return info;
   }
   // the static builds' grid rule (kernels.cu nll_shape): >= `waves` waves of resident CTAs
+  const int stile = kJitThreads * spec_tile().e;
+  ntl = (n + stile - 1) / stile;
+  if (ntl < 1) ntl = 1;
+  ntiles = static_cast<int>(ntl);
   const long long slots = static_cast<long long>(device_sm_count()) * m->occ;
   long long want = (waves * slots + ntiles - 1) / ntiles;
   if (want < 1) want = 1;
@@ -1077,14 +1103,14 @@ NllLaunchInfo launch_nll_spec(const DevPlan& launch, const ColPtrs& cols, long l
   if (ev_start) cudaEventRecord(ev_start, stream);
   const CUresult rc =
       drv.launch(m->fn, static_cast<unsigned>(static_cast<long long>(ntiles) * nchunks), 1, 1, kJitThreads, 1, 1,
-                 (launch.ncols + launch.ncached) * kJitTile * sizeof(double),
+                 (launch.ncols + launch.ncached) * stile * sizeof(double),
                  reinterpret_cast<CUstream>(stream), args, nullptr);
   if (ev_stop) cudaEventRecord(ev_stop, stream);
   if (rc != CUDA_SUCCESS) numeric_error("cuLaunchKernel (plan-specialised likelihood) failed: " + std::to_string(rc));
   launch_reduce(partial, ntiles, P, d_out, stream);
   info.threads = kJitThreads;
-  info.events_per_thread = kJitE;
-  info.tile = kJitTile;
+  info.events_per_thread = spec_tile().e;
+  info.tile = stile;
   info.ntiles = ntiles;
   info.nchunks = nchunks;
   info.grid = ntiles * nchunks;
