@@ -869,3 +869,42 @@ def test_few_point_calls_replay_a_cuda_graph():
     v3 = [fb.nll_points(m, ds, bad)[0][0] for _ in range(3)]
     _, comp3, _ = o.nll(cols, bad[0])
     assert v3[0] == v3[1] == v3[2] and abs(v3[0] - comp3) <= NLL_TOL * abs(comp3)
+
+
+def test_distinct_models_on_distinct_threads():
+    """SPEC.md: a model is single-owner, distinct models may run on distinct threads.  Four
+    host threads, each with its own model (native and formula spellings), run single-point
+    calls (CUDA-graph replay) and 16-point launches (run-time compiled builds) at once;
+    every value equals the one-thread run bit for bit."""
+    import threading
+    w = configs.C2
+    texts = [w.text, configs.REFERENCE_TEXTS[w.name], w.text, configs.REFERENCE_TEXTS[w.name]]
+    mo = fb.Model.from_string(w.text)
+    cols, _ = fb.sample_host(mo, 200_003, 23)
+    ds = fb.DataSet.from_columns(cols)
+    base = [dict(zip(mo.param_names, r)) for r in w.points(mo, n_points=16)]
+
+    def work(text):
+        m = fb.Model.from_string(text)
+        pts = np.array([[d[n] for n in m.param_names] for d in base])
+        out = [fb.nll_points(m, ds, pts[i:i + 1])[0][0] for i in range(4) for _ in range(3)]
+        out += list(fb.nll_points(m, ds, pts)[0])
+        return out
+
+    want = [work(t) for t in texts]
+    got = [None] * len(texts)
+    errors = []
+
+    def run(i):
+        try:
+            got[i] = work(texts[i])
+        except Exception as e:  # reported below
+            errors.append(e)
+
+    threads = [threading.Thread(target=run, args=(i,)) for i in range(len(texts))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    assert got == want
