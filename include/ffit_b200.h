@@ -254,7 +254,8 @@ int ffcu_fit_gradient(ffit_model* m, const ffit_dataset* ds, double tolerance,
 /* analytic = 1: gradients from the fused NLL + gradient pass when the model's
  * layout fits it, 0: central finite differences, -1 (ffcu_fit_gradient's default):
  * analytic except for models with Expression pdfs while their formula-specialised
- * likelihood builds are on (2d+1 points of those beat the interpreter's gradient pass). */
+ * likelihood builds are on (their normalisation derivatives are host quadratures, and
+ * 2d+1 points of the specialised build are faster). */
 int ffcu_fit_gradient_opts(ffit_model* m, const ffit_dataset* ds, double tolerance,
                            long max_iterations, int analytic, ffit_fit_result** out);
 /* 1 if the fit's gradients came from the fused pass. */

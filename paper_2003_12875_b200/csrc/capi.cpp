@@ -953,10 +953,11 @@ FFB_API int ffcu_fit_gradient_opts(ffit_model* m, const ffit_dataset* ds, double
     ffb::FitOptions o;
     o.record_trace = true;
     if (analytic < 0) {
-      // automatic: analytic gradients, except for models with Expression pdfs when their
-      // formula-specialised likelihood builds are on -- the gradient pass runs those
-      // formulas on the device interpreter, and 2d+1 points of the specialised build are
-      // faster (tools/expr_grad_bench.py: 0.9 vs 3.6 ms per gradient on the config-2 text)
+      // automatic: analytic gradients, except for models with Expression pdfs while their
+      // formula-specialised likelihood builds are on: the gradient of a Simpson-normalised
+      // formula needs host quadratures of its derivative every call, and 2d+1 points of
+      // the specialised build are faster (tools/expr_grad_bench.py: 0.87 vs 1.6 ms per
+      // gradient on the config-2 text with m0 free, fit 0.012 vs 0.16 s)
       o.analytic_gradient = engine(m).likelihood_plan().programs.empty() || !ffb::jit_enabled();
     } else {
       o.analytic_gradient = analytic != 0;

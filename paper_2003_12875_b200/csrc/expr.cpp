@@ -344,7 +344,18 @@ double ExprProgram::eval(const double* vars) const {
 }
 
 double ExprProgram::eval_dual(const double* vars, const double* dvars, double* dvalue) const {
-  std::vector<double> st(max_depth > 0 ? max_depth : 1), sd(st.size());
+  // the quadrature of a normalisation derivative calls this thousands of times: no heap
+  // allocation below 32 stack entries
+  double st_small[32], sd_small[32];
+  std::vector<double> st_big, sd_big;
+  double* st = st_small;
+  double* sd = sd_small;
+  if (max_depth > 32) {
+    st_big.resize(max_depth);
+    sd_big.resize(max_depth);
+    st = st_big.data();
+    sd = sd_big.data();
+  }
   int top = 0;
   for (const ExprInstr& in : code) {
     switch (in.op) {

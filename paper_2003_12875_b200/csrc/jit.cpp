@@ -4,6 +4,7 @@
 #include <dlfcn.h>
 #include <nvrtc.h>  // NVRTC types only: the library is dlopen'ed
 
+#include <algorithm>
 #include <atomic>
 #include <cstdint>
 #include <type_traits>
@@ -372,6 +373,87 @@ void emit_formula(std::ostream& o, const std::vector<ExprInstr>& prog, int off,
   o << "}\n";
 }
 
+// The forward-mode tangent of a formula (the analytic gradient of Expression leaves in the
+// plan-specialised gradient pass): d value / d t for the variables whose slot bit is set in
+// `seed` moving by t; values and tangents per event, libdevice math (accuracy, not bits:
+// the pass's NLL slot comes from the leaf values of pass 1).
+void emit_tangent(std::ostream& o, const std::vector<ExprInstr>& prog, int off, const std::string& name) {
+  std::ostringstream b;
+  int depth = 0, max_depth = 0;
+  auto V = [](int d) { return "v" + std::to_string(d) + "[e]"; };
+  auto T = [](int d) { return "t" + std::to_string(d) + "[e]"; };
+  auto loop = [&](const std::string& stmt) {
+    b << "#pragma unroll\n  for (int e = 0; e < E; ++e) { " << stmt << " }\n";
+  };
+  const int end = program_end(prog, off);
+  for (int j = off; j < end; ++j) {
+    const ExprInstr& in = prog[j];
+    switch (in.op) {
+      case EX_CONST:
+        loop(V(depth) + " = " + hexbits(in.c) + "; " + T(depth) + " = 0.0;");
+        ++depth;
+        break;
+      case EX_VAR:
+        loop(V(depth) + " = k[" + std::to_string(1 + in.slot) + "]; " + T(depth) + " = ((seed >> " +
+             std::to_string(in.slot) + ") & 1) ? 1.0 : 0.0;");
+        ++depth;
+        break;
+      case EX_X:
+        loop(V(depth) + " = x[e]; " + T(depth) + " = 0.0;");
+        ++depth;
+        break;
+      case EX_ADD: case EX_SUB: case EX_MUL: case EX_DIV: case EX_POW: {
+        --depth;
+        const int l = depth - 1, r = depth;
+        const std::string a = V(l), bb = V(r), ta = T(l), tb = T(r);
+        if (in.op == EX_ADD) {
+          loop(a + " = " + a + " + " + bb + "; " + ta + " = " + ta + " + " + tb + ";");
+        } else if (in.op == EX_SUB) {
+          loop(a + " = " + a + " - " + bb + "; " + ta + " = " + ta + " - " + tb + ";");
+        } else if (in.op == EX_MUL) {
+          loop(ta + " = " + ta + " * " + bb + " + " + a + " * " + tb + "; " + a + " = " + a + " * " + bb + ";");
+        } else if (in.op == EX_DIV) {
+          loop("const double q = " + a + " / " + bb + "; " + ta + " = (" + ta + " - q * " + tb + ") / " + bb + "; " +
+               a + " = q;");
+        } else {
+          loop("const double r = ffb_pow(" + a + ", " + bb + "); " + ta + " = (" + ta + " != 0.0 ? " + bb +
+               " * pow(" + a + ", " + bb + " - 1.0) * " + ta + " : 0.0) + (" + tb + " != 0.0 ? r * log(" + a +
+               ") * " + tb + " : 0.0); " + a + " = r;");
+        }
+        break;
+      }
+      default: {
+        const int d = depth - 1;
+        const std::string a = V(d), t = T(d);
+        std::string r, g;  // value, derivative of the op at a
+        switch (in.op) {
+          case EX_NEG: r = "-a"; g = "-1.0"; break;
+          case EX_SQUARE: r = "a * a"; g = "2.0 * a"; break;
+          case EX_CUBE: r = "a * a * a"; g = "3.0 * a * a"; break;
+          case EX_FOURTH: r = "(a * a) * (a * a)"; g = "4.0 * a * a * a"; break;
+          case EX_EXP: r = "exp(a)"; g = "r"; break;
+          case EX_LOG: r = "log(a)"; g = "1.0 / a"; break;
+          case EX_SIN: r = "sin(a)"; g = "cos(a)"; break;
+          case EX_COS: r = "cos(a)"; g = "-sin(a)"; break;
+          case EX_SQRT: r = "sqrt(a)"; g = "0.5 / r"; break;
+          case EX_ABS: r = "fabs(a)"; g = "(a < 0.0 ? -1.0 : 1.0)"; break;
+          case EX_SINH: r = "sinh(a)"; g = "cosh(a)"; break;
+          default: r = "asinh(a)"; g = "1.0 / sqrt(a * a + 1.0)"; break;
+        }
+        loop("const double a = " + a + "; const double r = " + r + "; " + t + " = " + t + " != 0.0 ? (" + g +
+             ") * " + t + " : 0.0; " + a + " = r;");
+        break;
+      }
+    }
+    if (depth > max_depth) max_depth = depth;
+  }
+  o << "template <int E>\n__device__ __forceinline__ void " << name
+    << "(const double (&x)[E], const double* __restrict__ k, int seed, double (&dv)[E]) {\n"
+    << "  (void)x; (void)k; (void)seed;\n";
+  for (int d = 0; d < max_depth; ++d) o << "  double v" << d << "[E], t" << d << "[E];\n";
+  o << b.str() << "#pragma unroll\n  for (int e = 0; e < E; ++e) dv[e] = t0[e];\n}\n";
+}
+
 }  // namespace
 
 ExprHoist analyse_expr_hoist(const HostPlan& plan, const double* rows, int P) {
@@ -551,6 +633,7 @@ std::string jit_expression_source(const HostPlan& plan, const ExprHoist* hoist) 
     if (seen) continue;
     offsets.push_back(off);
     emit_formula(o, plan.programs, off, nullptr, "ffb_expr_" + std::to_string(off), false);
+    emit_tangent(o, plan.programs, off, "ffb_expr_" + std::to_string(off) + "_t");
     auto it = by_prog.find(off);
     if (it != by_prog.end()) {
       emit_formula(o, plan.programs, off, &it->second, "ffb_expr_" + std::to_string(off) + "_h", true);
@@ -561,6 +644,13 @@ std::string jit_expression_source(const HostPlan& plan, const ExprHoist* hoist) 
        "                                               double (&v)[E], const MathTables* __restrict__ tb) {\n"
        "  switch (off) {\n";
   for (const int off : offsets) o << "    case " << off << ": ffb_expr_" << off << "<E>(x, k, v, tb); break;\n";
+  o << "    default: break;\n  }\n}\n";
+  // the gradient pass's tangents (kernels_device.cuh leaf_grad, formula builds)
+  o << "template <int E>\n"
+       "__device__ __forceinline__ void ffb_expr_tangent(int off, const double* __restrict__ k, const double (&x)[E],\n"
+       "                                                 int seed, double (&dv)[E]) {\n"
+       "  switch (off) {\n";
+  for (const int off : offsets) o << "    case " << off << ": ffb_expr_" << off << "_t<E>(x, k, seed, dv); break;\n";
   o << "    default: break;\n  }\n}\n";
   if (hoist && !hoist->slots.empty()) {
     // the launch-constant subtrees: computed once per staged tile (nll_kernel) into
@@ -621,9 +711,18 @@ std::string grad_spec_source(const HostPlan& plan, const GradPlan& gp) {
     for (int i = 0; i < nt; ++i) a << (i ? ", " : "") << f(i);
     return a.str();
   };
+  if (!plan.programs.empty()) o << jit_expression_source(plan);  // the formulas and their tangents
+  int nseed = 0;
+  for (int i = 0; i < nt; ++i) {
+    if (plan.dev.t[i].kind == LK_EXPR) nseed = std::max(nseed, gp.dev.g[i].seeds + __builtin_popcount(gp.dev.g[i].pmask));
+  }
+  std::ostringstream seeds;
+  for (int i = 0; i < std::max(nseed, 1); ++i) seeds << (i ? ", " : "") << (i < nseed ? gp.dev.seed[i] : 0);
   o << "// generated by jit.cpp: the plan's term list and slot layout for nll_grad_spec_kernel\n"
        "namespace ffb {\nstruct GradSpec {\n"
     << "  static constexpr int nterms = " << nt << ";\n"
+    << "  static constexpr int seedoff[" << nt << "] = {" << arr([&](int i) { return gp.dev.g[i].seeds; }) << "};\n"
+    << "  static constexpr int seed[" << std::max(nseed, 1) << "] = {" << seeds.str() << "};\n"
     << "  static constexpr int kind[" << nt << "] = {" << arr([&](int i) { return plan.dev.t[i].kind; }) << "};\n"
     << "  static constexpr int order[" << nt << "] = {" << arr([&](int i) { return plan.dev.t[i].order; }) << "};\n"
     << "  static constexpr int pmask[" << nt << "] = {" << arr([&](int i) { return gp.dev.g[i].pmask; }) << "};\n"
@@ -679,9 +778,7 @@ bool grad_spec_compile_only(const HostPlan& plan, const GradPlan& gp, int ks, st
 }
 
 bool grad_spec_applies(const HostPlan& plan, const GradPlan& gp, const ColPtrs& cols, int P) {
-  if (!jit_enabled() || !gp.ok || P != 1 || !plan.dev.simple || plan.dev.ncols != 1 || !plan.programs.empty()) {
-    return false;
-  }
+  if (!jit_enabled() || !gp.ok || P != 1 || !plan.dev.simple || plan.dev.ncols != 1) return false;
   if (std::getenv("FFB_NO_GRAD_SPEC") || std::getenv("FFB_NO_STREAM")) return false;
   return (reinterpret_cast<uintptr_t>(cols.c[0]) & 15) == 0;
 }

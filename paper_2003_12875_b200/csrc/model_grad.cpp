@@ -133,13 +133,22 @@ double Model::eval_unnorm_1d_grad(int id, const double* theta, double x, int j) 
       if (p.children.size() == 1) return eval_unnorm_1d_grad(p.children[0], theta, x, j);
       usage_error("eval_unnorm_1d_grad: multi-observable ProdPdf");
     case Kind::Expression: {  // forward mode through the formula: every slot reading theta_j moves
-      std::vector<double> v(p.expr_vars.size()), dv(p.expr_vars.size());
+      double vs[16], dvs[16];
+      std::vector<double> vb, dvb;
+      double* v = vs;
+      double* dv = dvs;
+      if (p.expr_vars.size() > 16) {
+        vb.resize(p.expr_vars.size());
+        dvb.resize(p.expr_vars.size());
+        v = vb.data();
+        dv = dvb.data();
+      }
       for (std::size_t i = 0; i < p.expr_vars.size(); ++i) {
         v[i] = p.expr_vars[i] < 0 ? x : theta[p.expr_vars[i]];
         dv[i] = p.expr_vars[i] == j ? 1.0 : 0.0;
       }
       double d = 0.0;
-      p.program->eval_dual(v.data(), dv.data(), &d);
+      p.program->eval_dual(v, dv, &d);
       return d;
     }
   }

@@ -22,6 +22,7 @@ free = [k for k, nm in enumerate(m.param_names) if not m.is_constant(nm)]
 for i, k in enumerate(free):
     pts[1 + 2 * i, k] += 1e-6; pts[2 + 2 * i, k] -= 1e-6
 for f, name in ((lambda: fb.nll_grad(m, ds, th), "analytic grad"), (lambda: fb.nll_points(m, ds, pts), f"FD {len(pts)} pts")):
+    f(); print(name, "spec build:", fb.last_grad_jit(m), "status:", fb.expression_jit_status()[:300])
     for _ in range(3): f()
     torch.cuda.synchronize(); t = time.perf_counter()
     for _ in range(10): f()
