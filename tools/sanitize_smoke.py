@@ -30,4 +30,35 @@ for jit in (False, True):
     fb.expression_jit(jit)
     fb.nll_points(m, ds, m.theta())
     fb.nll_points(m, ds, np.repeat(m.theta()[None, :], 10, axis=0))
+
+# the run-time compiled builds at small sizes (threshold 0): plan-specialised tile and
+# streaming kernels (one and three columns), the launch-constant caches (ArgusBG pair,
+# whole leaves), formula subtrees cached per tile, the formula gradient pass, and the
+# CUDA-graph replay of single-point calls
+fb.plan_spec_min_work(0)
+for w, n in ((configs.C2, 10_001), (configs.C3, 5_003), (configs.C4, 7_001)):
+    m = fb.Model.from_string(w.text)
+    cols, _ = fb.sample_host(m, n, 3)
+    ds = fb.DataSet.from_columns(cols)
+    pts = w.points(m, n_points=12)
+    if w is configs.C4:  # yields only: every leaf cached per tile
+        base = m.theta()
+        for k, name in enumerate(m.param_names):
+            if not name.startswith("n"):
+                pts[:, k] = base[k]
+    fb.nll_points(m, ds, pts)
+    fb.nll_points(m, ds, pts[:2])
+    for _ in range(3):
+        fb.nll_points(m, ds, pts[:1])  # plain, capture, replay
+    fb.nll_grad(m, ds, pts[0])
+ref = configs.REFERENCE_TEXTS[configs.C2.name]
+m = fb.Model.from_string(ref)
+mo = fb.Model.from_string(configs.C2.text)
+cols, _ = fb.sample_host(mo, 9_001, 4)
+ds = fb.DataSet.from_columns(cols)
+by = [dict(zip(mo.param_names, r)) for r in configs.C2.points(mo, n_points=12)]
+pts = np.array([[d[k] for k in m.param_names] for d in by])
+fb.nll_points(m, ds, pts)            # formula build with cached subtrees
+mf = fb.Model.from_string(ref.replace("parameter m0 5.291 5.0 5.4 const", "parameter m0 5.291 5.2901 5.30"))
+fb.nll_grad(mf, ds, mf.theta())      # plan-specialised gradient pass with formula tangents
 print("sanitize smoke done")
