@@ -346,7 +346,7 @@ double ExprProgram::eval(const double* vars) const {
 double ExprProgram::eval_dual(const double* vars, const double* dvars, double* dvalue) const {
   // the quadrature of a normalisation derivative calls this thousands of times: no heap
   // allocation below 32 stack entries
-  double st_small[32], sd_small[32];
+  double st_small[32] = {0.0}, sd_small[32] = {0.0};
   std::vector<double> st_big, sd_big;
   double* st = st_small;
   double* sd = sd_small;
