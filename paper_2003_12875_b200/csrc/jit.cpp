@@ -693,8 +693,18 @@ namespace {
 // ---------------------------------------------------------------------------
 // plan-specialised gradient pass (kernels_device.cuh nll_grad_spec_kernel)
 
-constexpr int kSpecE = 8;
-constexpr int kSpecTile = kJitThreads * kSpecE;
+// events per thread and pipeline stages of the plan-specialised gradient pass: single-column
+// single sums keep 8 events per thread and three stages; multi-column / product plans hold
+// the factor sums per event too, so 4 events and two stages (nll_grad_spec_kernel)
+constexpr int kGradSpecMaxCols = 3;
+int grad_spec_e(const DevPlan& d) { return d.simple && d.ncols == 1 ? 8 : 4; }
+int grad_spec_smem(const DevPlan& d) {
+  return (d.ncols == 1 ? kJitStages : 2) * d.ncols * kJitThreads * grad_spec_e(d) * static_cast<int>(sizeof(double));
+}
+std::string grad_spec_name(const DevPlan& d, int ks) {
+  return "&ffb::nll_grad_spec_kernel<" + std::to_string(kJitThreads) + ", " + std::to_string(grad_spec_e(d)) + ", " +
+         std::to_string(ks) + ">";
+}
 
 struct SpecModule {
   CUmodule mod = nullptr;
@@ -727,7 +737,16 @@ std::string grad_spec_source(const HostPlan& plan, const GradPlan& gp) {
     << "  static constexpr int order[" << nt << "] = {" << arr([&](int i) { return plan.dev.t[i].order; }) << "};\n"
     << "  static constexpr int pmask[" << nt << "] = {" << arr([&](int i) { return gp.dev.g[i].pmask; }) << "};\n"
     << "  static constexpr int aslot[" << nt << "] = {" << arr([&](int i) { return gp.dev.g[i].slot; }) << "};\n"
-    << "  static constexpr int nslots = " << gp.dev.nslots << ";\n};\n}  // namespace ffb\n"
+    << "  static constexpr int nslots = " << gp.dev.nslots << ";\n"
+    << "  static constexpr int ncols = " << plan.dev.ncols << ";\n"
+    << "  static constexpr bool simple = " << (plan.dev.simple ? "true" : "false") << ";\n"
+    << "  static constexpr int nfactors = " << gp.dev.nfactors << ";\n"
+    << "  static constexpr int col[" << nt << "] = {" << arr([&](int i) { return plan.dev.t[i].col; }) << "};\n"
+    << "  static constexpr int flags[" << nt << "] = {" << arr([&](int i) { return plan.dev.t[i].flags; }) << "};\n"
+    << "  static constexpr int factor[" << nt << "] = {" << arr([&](int i) { return gp.dev.g[i].factor; }) << "};\n"
+    << "  static constexpr int fbeg[" << nt << "] = {" << arr([&](int i) { return gp.dev.g[i].fbeg; }) << "};\n"
+    << "  static constexpr int fend[" << nt << "] = {" << arr([&](int i) { return gp.dev.g[i].fend; }) << "};\n"
+    << "};\n}  // namespace ffb\n"
     << "#define FFB_GRAD_SPEC 1\n#include \"kernels_device.cuh\"\n";
   return o.str();
 }
@@ -742,8 +761,7 @@ SpecModule* spec_module(const HostPlan& plan, const GradPlan& gp, int ks) {
   if (it != g_spec.end()) return it->second.mod ? &it->second : nullptr;
   SpecModule m;
   DriverApi& drv = driver();
-  const std::string name = "&ffb::nll_grad_spec_kernel<" + std::to_string(kJitThreads) + ", " +
-                           std::to_string(kSpecE) + ", " + std::to_string(ks) + ">";
+  const std::string name = grad_spec_name(plan.dev, ks);
   std::vector<char> cubin;
   std::vector<std::string> lowered;
   std::string log;
@@ -751,7 +769,7 @@ SpecModule* spec_module(const HostPlan& plan, const GradPlan& gp, int ks) {
     cudaFree(nullptr);
     if (drv.module_load(&m.mod, cubin.data()) == CUDA_SUCCESS &&
         drv.get_function(&m.fn, m.mod, lowered[0].c_str()) == CUDA_SUCCESS) {
-      const int smem = kJitStages * kSpecTile * static_cast<int>(sizeof(double));
+      const int smem = grad_spec_smem(plan.dev);
       drv.set_attribute(m.fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem);
       drv.occupancy(&m.occ, m.fn, kJitThreads, smem);
       if (m.occ < 1) m.occ = 1;
@@ -772,15 +790,16 @@ std::string grad_spec_text(const HostPlan& plan, const GradPlan& gp) { return gr
 bool grad_spec_compile_only(const HostPlan& plan, const GradPlan& gp, int ks, std::string* log) {
   std::vector<char> cubin;
   std::vector<std::string> low;
-  const std::string name = "&ffb::nll_grad_spec_kernel<" + std::to_string(kJitThreads) + ", " +
-                           std::to_string(kSpecE) + ", " + std::to_string(ks) + ">";
-  return compile(grad_spec_source(plan, gp), {name}, &cubin, &low, log);
+  return compile(grad_spec_source(plan, gp), {grad_spec_name(plan.dev, ks)}, &cubin, &low, log);
 }
 
 bool grad_spec_applies(const HostPlan& plan, const GradPlan& gp, const ColPtrs& cols, int P) {
-  if (!jit_enabled() || !gp.ok || P != 1 || !plan.dev.simple || plan.dev.ncols != 1) return false;
+  if (!jit_enabled() || !gp.ok || P != 1 || plan.dev.ncols > kGradSpecMaxCols) return false;
   if (std::getenv("FFB_NO_GRAD_SPEC") || std::getenv("FFB_NO_STREAM")) return false;
-  return (reinterpret_cast<uintptr_t>(cols.c[0]) & 15) == 0;
+  for (int c = 0; c < plan.dev.ncols; ++c) {
+    if (reinterpret_cast<uintptr_t>(cols.c[c]) & 15) return false;
+  }
+  return true;
 }
 
 bool grad_spec_prepare(const HostPlan& plan, const GradPlan& gp, int ks) {
@@ -795,7 +814,8 @@ NllLaunchInfo launch_nll_grad_spec(const HostPlan& plan, const GradPlan& gp, con
   SpecModule* m = spec_module(plan, gp, ks);
   if (!m) usage_error("internal: launch_nll_grad_spec without a module");
   DriverApi& drv = driver();
-  const long long ntl = (n + kSpecTile - 1) / kSpecTile;
+  const int stile = kJitThreads * grad_spec_e(plan.dev);
+  const long long ntl = (n + stile - 1) / stile;
   long long G = static_cast<long long>(device_sm_count()) * m->occ;
   if (G > ntl) G = ntl;
   DevPlan dp = plan.dev;
@@ -808,15 +828,14 @@ NllLaunchInfo launch_nll_grad_spec(const HostPlan& plan, const GradPlan& gp, con
   void* args[] = {&dp, &cp, &nn, &kc, &ntiles, &partial, &bad};
   cudaMemsetAsync(d_bad, 0xff, sizeof(unsigned long long), stream);
   if (ev_start) cudaEventRecord(ev_start, stream);
-  const CUresult rc = drv.launch(m->fn, static_cast<unsigned>(G), 1, 1, kJitThreads, 1, 1,
-                                 kJitStages * kSpecTile * sizeof(double), reinterpret_cast<CUstream>(stream), args,
-                                 nullptr);
+  const CUresult rc = drv.launch(m->fn, static_cast<unsigned>(G), 1, 1, kJitThreads, 1, 1, grad_spec_smem(plan.dev),
+                                 reinterpret_cast<CUstream>(stream), args, nullptr);
   if (ev_stop) cudaEventRecord(ev_stop, stream);
   if (rc != CUDA_SUCCESS) numeric_error("cuLaunchKernel (plan-specialised gradient) failed: " + std::to_string(rc));
   launch_reduce(partial, static_cast<int>(G), gp.dev.nslots, d_out, stream);
   info.threads = kJitThreads;
-  info.events_per_thread = kSpecE;
-  info.tile = kSpecTile;
+  info.events_per_thread = grad_spec_e(plan.dev);
+  info.tile = stile;
   info.ntiles = static_cast<int>(ntl);
   info.grid = static_cast<int>(G);
   info.launches = 2;

@@ -289,10 +289,12 @@ def test_sharded_gradient_single_rank_equals_direct():
     assert np.allclose(g[0], g0[0], rtol=1e-14, atol=0)
 
 
-@pytest.mark.parametrize("name", ["c2_gauss_argus", "c5_m0_free", "c4_extended", "c1_gauss"])
+@pytest.mark.parametrize("name", ["c2_gauss_argus", "c5_m0_free", "c4_extended", "c1_gauss", "c3_product",
+                                  "sum_of_products", "prod_first_sum", "mix3_nested"])
 def test_plan_specialised_gradient_pass(name, monkeypatch):
-    """One-point gradients of single-column models run the plan-specialised (NVRTC) pass;
-    it agrees with the generic pass and with the oracle-referenced gradient."""
+    """One-point gradients run the plan-specialised (NVRTC) pass -- single-column sums and
+    products over up to three observables; it agrees with the generic pass and with the
+    oracle-referenced gradient."""
     text, n = CASES[name]
     m, ds, cols = setup(text, n)
     th = jittered(m, text, seed=7)
