@@ -265,6 +265,20 @@ void Engine::bind_columns(const HostPlan& plan, const DeviceDataset& ds, ColPtrs
 
 const double* Engine::upload_constants(const HostPlan& plan, const double* thetas, int P,
                                        cudaStream_t s, double extra_scale) {
+  const int k = build_rows(plan, thetas, P, extra_scale);
+  return copy_rows(plan, k, P, s);
+}
+
+const double* Engine::copy_rows(const HostPlan& plan, int k, int P, cudaStream_t s) {
+  cuda_check(cudaMemcpyAsync(d_consts_[k], h_consts_[k],
+                             static_cast<std::size_t>(P) * plan.dev.stride * sizeof(double),
+                             cudaMemcpyHostToDevice, s),
+             "cudaMemcpyAsync(consts)");
+  cuda_check(cudaEventRecord(staged_[k], s), "cudaEventRecord");
+  return d_consts_[k];
+}
+
+int Engine::build_rows(const HostPlan& plan, const double* thetas, int P, double extra_scale) {
   const int k = slot_ ^= 1;
   // slot k fed the copy two calls ago; that copy must be done before reuse
   cuda_check(cudaEventSynchronize(staged_[k]), "cudaEventSynchronize");
@@ -286,12 +300,7 @@ const double* Engine::upload_constants(const HostPlan& plan, const double* theta
   } else {
     for (int p = 1; p < P; ++p) row(p);
   }
-  cuda_check(cudaMemcpyAsync(d_consts_[k], h_consts_[k],
-                             static_cast<std::size_t>(P) * stride * sizeof(double),
-                             cudaMemcpyHostToDevice, s),
-             "cudaMemcpyAsync(consts)");
-  cuda_check(cudaEventRecord(staged_[k], s), "cudaEventRecord");
-  return d_consts_[k];
+  return k;
 }
 
 int Engine::nll_points_device(const DeviceDataset& ds, const double* thetas, int P,
@@ -310,8 +319,11 @@ int Engine::nll_points_device(const DeviceDataset& ds, const double* thetas, int
     cudaStreamWaitEvent(s, ev, 0);
     cudaEventDestroy(ev);
   }
-  // the likelihood kernel evaluates p * 2^kPScaleLog2 (plan.hpp)
-  const double* d_consts = upload_constants(plan_, thetas, P, s, std::ldexp(1.0, kPScaleLog2));
+  // the likelihood kernel evaluates p * 2^kPScaleLog2 (plan.hpp); the launch decisions
+  // (launch-constant caches may flag rows) come between building the rows and their copy
+  const int slot = build_rows(plan_, thetas, P, std::ldexp(1.0, kPScaleLog2));
+  const LaunchChoice choice = choose_launch(h_consts_[slot], P, ds.n);
+  const double* d_consts = copy_rows(plan_, slot, P, s);
   cudaEvent_t ea = nullptr, eb = nullptr;
   {
     std::lock_guard<std::mutex> lk(g_timer_mu);
@@ -321,7 +333,7 @@ int Engine::nll_points_device(const DeviceDataset& ds, const double* thetas, int
       g_timer_events.emplace_back(ea, eb);
     }
   }
-  const int launches = launch_device(ds, P, d_consts, h_consts_[slot_], d_pairs, d_bad, s, ea, eb);
+  const int launches = launch_device(ds, P, d_consts, h_consts_[slot], choice, d_pairs, d_bad, s, ea, eb);
   if (s != stream_) {
     cudaEvent_t ev;
     cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
@@ -333,9 +345,24 @@ int Engine::nll_points_device(const DeviceDataset& ds, const double* thetas, int
   return launches;
 }
 
+Engine::LaunchChoice Engine::choose_launch(double* h_rows, int P, long long n) {
+  LaunchChoice c;
+  c.lp = plan_.dev;
+  if (!plan_.programs.empty() && jit_prepare(plan_)) {
+    c.jit = true;  // Expression leaves: the formula-specialised build (jit.cpp)
+    return c;
+  }
+  // launch-constant branches (leaves / ArgusBG data parts fixed over the launch) cached per
+  // tile; a partly shared ArgusBG m0 flags the rows that use the cache
+  c.cached = cache_launch_constants(c.lp, h_rows, P);
+  c.ks = plan_kind_set(c.lp, h_rows, P);
+  c.spec = plan_spec_applies(plan_, c.lp, n, P) && plan_spec_prepare(c.lp, c.ks);
+  return c;
+}
+
 int Engine::launch_device(const DeviceDataset& ds, int P, const double* d_consts, const double* h_rows,
-                          SumPair* d_pairs, unsigned long long* d_bad, cudaStream_t s, cudaEvent_t ea,
-                          cudaEvent_t eb) {
+                          const LaunchChoice& c, SumPair* d_pairs, unsigned long long* d_bad, cudaStream_t s,
+                          cudaEvent_t ea, cudaEvent_t eb) {
   if (ds.n == 0) {
     cuda_check(cudaMemsetAsync(d_pairs, 0, P * sizeof(SumPair), s), "cudaMemsetAsync");
     cuda_check(cudaMemsetAsync(d_bad, 0xff, P * sizeof(unsigned long long), s), "cudaMemsetAsync");
@@ -343,21 +370,17 @@ int Engine::launch_device(const DeviceDataset& ds, int P, const double* d_consts
   }
   ColPtrs cols;
   bind_columns(plan_, ds, cols);
-  if (!plan_.programs.empty() && jit_prepare(plan_)) {
-    // Expression leaves: the formula-specialised build (jit.cpp) instead of the interpreter
+  if (c.jit) {
     last_ = launch_nll_jit(plan_, cols, ds.n, d_consts, P, d_scratch_, d_pairs, d_bad, s, h_rows, ea, eb);
   } else {
-    // launch-constant branches (ArgusBG with m0 fixed over the launch) cached per tile
-    DevPlan lp = plan_.dev;
-    const int cached = cache_launch_constants(lp, h_rows, P);
-    const int ks = plan_kind_set(lp, h_rows, P);
-    if (plan_spec_applies(plan_, lp, ds.n, P) && plan_spec_prepare(lp, ks)) {
+    if (c.spec) {
       // the tile kernel compiled around this launch's term list (jit.cpp; cached)
-      last_ = launch_nll_spec(lp, cols, ds.n, d_consts, P, d_scratch_, d_pairs, d_bad, s, ks, nll_waves(), ea, eb);
+      last_ = launch_nll_spec(c.lp, cols, ds.n, d_consts, P, d_scratch_, d_pairs, d_bad, s, c.ks, nll_waves(), ea,
+                              eb);
     } else {
-      last_ = launch_nll(lp, cols, ds.n, d_consts, P, d_scratch_, d_pairs, d_bad, s, ks, ea, eb);
+      last_ = launch_nll(c.lp, cols, ds.n, d_consts, P, d_scratch_, d_pairs, d_bad, s, c.ks, ea, eb);
     }
-    last_.cached = cached;
+    last_.cached = c.cached;
   }
   cuda_check(cudaGetLastError(), "launch_nll");
   return last_.launches;
@@ -365,19 +388,19 @@ int Engine::launch_device(const DeviceDataset& ds, int P, const double* d_consts
 
 // What launch_device would run for these rows: the key under which a captured graph of
 // the launch stays valid (the dataset's columns and size, P, and every launch decision).
-std::string Engine::launch_signature(const DeviceDataset& ds, int P, const double* h_rows) const {
+std::string Engine::launch_signature(const DeviceDataset& ds, int P, const LaunchChoice& c,
+                                     const double* h_rows) const {
   std::ostringstream o;
   o << ds.n << ':' << P;
-  for (const double* c : ds.cols) o << ':' << static_cast<const void*>(c);
-  if (!plan_.programs.empty()) {
+  for (const double* col : ds.cols) o << ':' << static_cast<const void*>(col);
+  if (c.jit) {
     const ExprHoist h = analyse_expr_hoist(plan_, h_rows, P);
-    o << "|jit" << jit_enabled();
+    o << "|jit";
     for (const HoistSlot& v : h.slots) o << ',' << v.col << '/' << v.begin << '/' << v.end;
   } else {
-    DevPlan lp = plan_.dev;
-    o << "|c" << cache_launch_constants(lp, h_rows, P) << "|k" << plan_kind_set(lp, h_rows, P) << "|s"
-      << plan_spec_applies(plan_, lp, ds.n, P);
-    for (int i = 0; i < lp.nterms; ++i) o << ',' << lp.t[i].kind << '/' << lp.t[i].order;
+    o << "|c" << c.cached << "|k" << c.ks << "|s" << c.spec;
+    for (int i = 0; i < c.lp.nterms; ++i) o << ',' << c.lp.t[i].kind << '/' << c.lp.t[i].order;
+    for (int d = 0; d < c.lp.nderived; ++d) o << ",d" << c.lp.dv[d].row << '/' << c.lp.dv[d].dst;
   }
   return o.str();
 }
@@ -419,12 +442,13 @@ NllResult Engine::nll_points_graph(const DeviceDataset& ds, const double* thetas
     build_constants(plan_, m_, thetas + static_cast<std::size_t>(p) * npar,
                     h_consts_[0] + static_cast<std::size_t>(p) * stride, std::ldexp(1.0, kPScaleLog2));
   }
-  const std::string key = launch_signature(ds, P, h_consts_[0]);
+  const LaunchChoice choice = choose_launch(h_consts_[0], P, ds.n);
+  const std::string key = launch_signature(ds, P, choice, h_consts_[0]);
   const std::size_t bytes = static_cast<std::size_t>(P) * stride * sizeof(double);
   auto sequence = [&] {
     cuda_check(cudaMemcpyAsync(d_consts_[0], h_consts_[0], bytes, cudaMemcpyHostToDevice, stream_),
                "cudaMemcpyAsync(consts)");
-    launch_device(ds, P, d_consts_[0], h_consts_[0], d_pairs_, d_bad_, stream_, nullptr, nullptr);
+    launch_device(ds, P, d_consts_[0], h_consts_[0], choice, d_pairs_, d_bad_, stream_, nullptr, nullptr);
     cuda_check(cudaMemcpyAsync(h_pairs_, d_pairs_, P * sizeof(SumPair), cudaMemcpyDeviceToHost, stream_),
                "cudaMemcpyAsync(pairs)");
     cuda_check(cudaMemcpyAsync(h_bad_, d_bad_, P * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream_),

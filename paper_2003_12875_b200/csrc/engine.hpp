@@ -124,9 +124,20 @@ class Engine {
   static constexpr int kGraphMaxPoints = 8;  // few-point synchronous calls replay a CUDA graph
   NllResult nll_points_graph(const DeviceDataset& ds, const double* thetas, int P);
   NllResult nll_points_stream(const DeviceDataset& ds, const double* thetas, int P);
-  int launch_device(const DeviceDataset& ds, int P, const double* d_consts, const double* h_rows, SumPair* d_pairs,
-                    unsigned long long* d_bad, cudaStream_t s, cudaEvent_t ea, cudaEvent_t eb);
-  std::string launch_signature(const DeviceDataset& ds, int P, const double* h_rows) const;
+  // the kernel build and plan rewrite a launch of these rows takes (may flag rows for the
+  // partly shared ArgusBG cache, so it runs between building and copying them)
+  struct LaunchChoice {
+    DevPlan lp{};
+    int cached = 0, ks = 0;
+    bool jit = false, spec = false;
+  };
+  LaunchChoice choose_launch(double* h_rows, int P, long long n);
+  int build_rows(const HostPlan& plan, const double* thetas, int P, double extra_scale);  // -> slot
+  const double* copy_rows(const HostPlan& plan, int slot, int P, cudaStream_t s);
+  int launch_device(const DeviceDataset& ds, int P, const double* d_consts, const double* h_rows,
+                    const LaunchChoice& c, SumPair* d_pairs, unsigned long long* d_bad, cudaStream_t s,
+                    cudaEvent_t ea, cudaEvent_t eb);
+  std::string launch_signature(const DeviceDataset& ds, int P, const LaunchChoice& c, const double* h_rows) const;
   void drop_graph();
   void bind_columns(const HostPlan& plan, const DeviceDataset& ds, ColPtrs& cols) const;
   void ensure(int device, int P, std::size_t scratch);

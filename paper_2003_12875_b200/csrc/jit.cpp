@@ -1113,9 +1113,10 @@ std::string plan_spec_struct(const DevPlan& d) {
     << (d.nderived > 0 ? d.nderived : 1) << "] = {";
   for (int i = 0; i < d.nderived; ++i) {
     const DevDerive& v = d.dv[i];
-    o << (i ? ", " : "") << "{" << v.col << ", " << v.coff << ", " << v.kind << ", " << v.order << ", " << v.dst << "}";
+    o << (i ? ", " : "") << "{" << v.col << ", " << v.coff << ", " << v.kind << ", " << v.order << ", " << v.dst << ", "
+      << v.row << "}";
   }
-  if (d.nderived == 0) o << "{0, 0, 0, 0, 0}";
+  if (d.nderived == 0) o << "{0, 0, 0, 0, 0, 0}";
   o << "};\n};\n}  // namespace ffb\n";
   return o.str();
 }

@@ -60,7 +60,9 @@ int plan_kind_set(const DevPlan& plan, const double* host_consts, int P);
 // into LK_ARGUS_CACHED terms whose data-only part the tile kernel computes once per
 // tile.  Values are bit-identical to the uncached plan.  Returns the terms rewritten
 // (0 when P is small enough for the streaming build, or FFB_NO_CONST_CACHE is set).
-int cache_launch_constants(DevPlan& plan, const double* host_consts, int P);
+// A majority m0 (at least half the points and more than kStreamMaxP) makes the term
+// LK_ARGUS_HYBRID instead: the rows of the points sharing it get the cache flag (c[5] = 1).
+int cache_launch_constants(DevPlan& plan, double* host_consts, int P);
 
 // Per-event values of the plan for one point (probabilities() when the plan is
 // normalised, PdfSpec::eval_batch when not).

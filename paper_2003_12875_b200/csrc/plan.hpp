@@ -33,7 +33,7 @@ enum LeafKind : int {
   LK_EXPO = 1,     // c: [coef, c]
   LK_CHISQ = 2,    // c: [coef, k/2 - 1, at_zero]
   LK_JOHNSON = 3,  // c: [coef, mu, 1/lambda, gamma, delta, delta/(lambda sqrt(2 pi))]
-  LK_ARGUS = 4,    // c: [coef, m0, c, p, 1/m0]
+  LK_ARGUS = 4,    // c: [coef, m0, c, p, 1/m0, cache flag]
   LK_CHEB = 5,     // c: [coef, lo+hi, 1/(hi-lo), a1..an]
   LK_POLY = 6,     // c: [coef, a1..an]
   LK_EXPR = 7,     // c: [coef, v_0..v_{k-1}] (the formula's parameter values); order = program
@@ -44,6 +44,9 @@ enum LeafKind : int {
   LK_LEAF_CACHED = 9,   // c: as the original leaf (only coef is read); order = shared-memory
                         // column of the tile's cached leaf values: every shape parameter of
                         // the leaf the same for every point of the launch (a yield-only fit)
+  LK_ARGUS_HYBRID = 10, // as LK_ARGUS_CACHED for the points whose cache flag (c[5]) is set --
+                        // most of the launch shares m0 and p = 1/2, e.g. a finite-difference
+                        // batch where two points move m0 -- and LK_ARGUS for the others
 };
 
 // Expression programs (expr.hpp): postfix instructions, END-terminated on the device.
@@ -117,6 +120,7 @@ struct DevDerive {
   int kind;  // LK_ARGUS_CACHED: the ArgusBG (t, u) pair; else the cached leaf's kind
   int order; // the cached leaf's order (Chebychev / Polynomial)
   int dst;   // first shared-memory column written
+  int row;   // the launch point whose constants the cache is computed from
 };
 
 struct DevPlan {

@@ -77,6 +77,7 @@ struct Emitter {
         consts.push_back(par(p, 1));
         consts.push_back(par(p, 2));
         consts.push_back(theta ? 1.0 / par(p, 0) : 0.0);  // hoisted reciprocal of m0
+        consts.push_back(0.0);  // launch-constant cache flag (kernels.cu cache_launch_constants)
         break;
       case Kind::Chebychev: {
         t.kind = LK_CHEB;

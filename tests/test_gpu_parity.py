@@ -106,7 +106,7 @@ def test_points_are_independent_of_batching():
 
 def test_launch_constant_cache_is_bit_identical():
     """ArgusBG with m0 (and p = 1/2) fixed over a launch's points is served by the
-    per-tile launch-constant cache; adding one point with another m0 turns the cache
+    per-tile launch-constant cache; more points without a majority m0 turn the cache
     off for that launch.  The shared points' values are bitwise equal either way, and
     match the oracle."""
     w = configs.C2
@@ -116,8 +116,8 @@ def test_launch_constant_cache_is_bit_identical():
     assert np.all(pts[:, j] == pts[0, j])
     cached, bad, _ = fb.nll_points(m, ds, pts)
     assert fb.last_launch_cached(m) == 1
-    other = pts[:1].copy()
-    other[0, j] = pts[0, j] * (1 + 1e-4)
+    other = np.repeat(pts[:1], 17, axis=0)  # 17 more points, each with its own m0: no majority
+    other[:, j] = pts[0, j] * (1 + 1e-4 * np.arange(1, 18))
     plain, _, _ = fb.nll_points(m, ds, np.vstack([pts, other]))
     assert fb.last_launch_cached(m) == 0
     assert np.array_equal(cached, plain[:16])
@@ -785,10 +785,13 @@ def test_launch_constant_cache_every_leaf_kind(name):
         pts[p, j] = base[j] * (1.0 + 2e-4 * (p - 6)) if base[j] != 0 else 1e-4 * (p - 6)
     cached, bad, _ = fb.nll_points(m, ds, pts)
     ncached = fb.last_launch_cached(m)
-    other = base.copy()
-    for k in range(len(base)):  # constant parameters too (ArgusBG's m0 in config 2)
-        other[k] = base[k] * (1 + 1e-4) if base[k] != 0 else 1e-4
-    plain, _, _ = fb.nll_points(m, ds, np.vstack([pts, other[None, :]]))
+    # 13 more points moving every parameter (constant ones too: ArgusBG's m0 in config 2),
+    # each to its own value: no launch-constant part and no majority m0 left
+    other = np.repeat(base[None, :], 13, axis=0)
+    for i in range(13):
+        for k in range(len(base)):
+            other[i, k] = base[k] * (1 + 1e-4 * (i + 1)) if base[k] != 0 else 1e-4 * (i + 1)
+    plain, _, _ = fb.nll_points(m, ds, np.vstack([pts, other]))
     assert fb.last_launch_cached(m) == 0
     assert np.array_equal(cached, plain[:12]), (ncached, np.max(np.abs(cached - plain[:12]) / np.abs(plain[:12])))
     for p in (0, 11):
@@ -908,3 +911,34 @@ def test_distinct_models_on_distinct_threads():
         t.join()
     assert not errors, errors
     assert got == want
+
+
+def test_launch_constant_cache_partly_shared_m0():
+    """A finite-difference batch of the config-5 model (m0 free): 9 of 11 points share m0,
+    so ArgusBG's data-only part is cached per tile for them (flagged rows) and the two m0
+    steps evaluate the full leaf.  Bitwise equal to the same points in a launch without a
+    majority m0 (nothing cached), and to the oracle."""
+    w = configs.C5
+    m, ds, cols, o = setup(w.text, 120_011, 29)
+    th = m.theta()
+    free = [k for k, n in enumerate(m.param_names) if not m.is_constant(n)]
+    pts = [th.copy()]
+    for k in free:
+        for sgn in (1.0, -1.0):
+            r = th.copy()
+            r[k] += sgn * 1e-5 * max(abs(th[k]), 1.0)
+            pts.append(r)
+    pts = np.array(pts)
+    assert len(pts) == 11
+    hybrid, bad, _ = fb.nll_points(m, ds, pts)
+    assert fb.last_launch_cached(m) == 1
+    j = m.param_names.index("m0")
+    extra = np.repeat(th[None, :], 14, axis=0)
+    extra[:, j] = th[j] + 1e-4 * np.arange(1, 15)  # 14 distinct m0: no majority left
+    plain, _, _ = fb.nll_points(m, ds, np.vstack([pts, extra]))
+    assert fb.last_launch_cached(m) == 0
+    assert np.array_equal(hybrid, plain[:11])
+    for p in (0, 1, 2 * free.index(j) + 1, 10):
+        _, comp, ob = o.nll(cols, pts[p])
+        assert bad[p] == ob == -1
+        assert abs(hybrid[p] - comp) <= NLL_TOL * abs(comp)

@@ -145,7 +145,7 @@ def test_point_constants_fold_normalisations():
     assert row[1] == v["m"] and row[2] == -1.0 / (2.0 * v["s"] * v["s"])
     assert row[0] == pytest.approx((v["f"] / n_sig) / n_mod, rel=2e-16)
     assert row[3] == pytest.approx(((1 - v["f"]) / n_bkg) / n_mod, rel=2e-16)
-    assert list(row[4:]) == [v["m0"], v["c"], v["p"], 1.0 / v["m0"]]
+    assert list(row[4:]) == [v["m0"], v["c"], v["p"], 1.0 / v["m0"], 0.0]  # + the launch-cache flag
 
 
 @pytest.mark.parametrize("name", list(REF_MODELS) + list(EXPR_MODELS))
