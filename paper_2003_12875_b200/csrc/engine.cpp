@@ -405,6 +405,28 @@ std::string Engine::launch_signature(const DeviceDataset& ds, int P, const Launc
   return o.str();
 }
 
+void Engine::ensure_gslots(std::size_t need) {
+  if (need <= cap_gslots_) return;
+  cuda_check(cudaStreamSynchronize(stream_), "cudaStreamSynchronize");
+  cudaFree(d_gslots_);
+  cudaFreeHost(h_gslots_);
+  cuda_check(cudaMalloc(&d_gslots_, need * sizeof(SumPair)), "cudaMalloc(gslots)");
+  cuda_check(cudaHostAlloc(&h_gslots_, need * sizeof(SumPair), cudaHostAllocDefault), "cudaHostAlloc");
+  cap_gslots_ = need;
+}
+
+void Engine::reserve(const DeviceDataset& ds, int P_nll, int P_grad) {
+  DeviceGuard g(ds.device);
+  std::size_t scratch = 0;
+  if (ds.n > 0 && P_nll > 0) scratch = nll_scratch_bytes(ds.n, P_nll, plan_.dev.ncols);
+  if (ds.n > 0 && P_grad > 0) {
+    const GradPlan& gp = grad_plan();
+    if (gp.ok) scratch = std::max(scratch, nll_grad_scratch_bytes(ds.n, P_grad, plan_.dev, gp.dev));
+  }
+  ensure(ds.device, std::max(P_nll, P_grad), scratch);
+  if (P_grad > 0 && grad_plan().ok) ensure_gslots(static_cast<std::size_t>(P_grad) * grad_plan().dev.nslots);
+}
+
 void Engine::drop_graph() {
   if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
   graph_exec_ = nullptr;
@@ -598,14 +620,7 @@ NllGradResult Engine::nll_grad_points(const DeviceDataset& ds, const double* the
     const std::size_t scratch = ds.n > 0 ? nll_grad_scratch_bytes(ds.n, np, plan_.dev, gp.dev) : 0;
     ensure(ds.device, np, scratch);
     const std::size_t need = static_cast<std::size_t>(np) * S;
-    if (need > cap_gslots_) {
-      cuda_check(cudaStreamSynchronize(stream_), "cudaStreamSynchronize");
-      cudaFree(d_gslots_);
-      cudaFreeHost(h_gslots_);
-      cuda_check(cudaMalloc(&d_gslots_, need * sizeof(SumPair)), "cudaMalloc(gslots)");
-      cuda_check(cudaHostAlloc(&h_gslots_, need * sizeof(SumPair), cudaHostAllocDefault), "cudaHostAlloc");
-      cap_gslots_ = need;
-    }
+    ensure_gslots(need);
     const double* d_consts = upload_constants(plan_, th, np, stream_, std::ldexp(1.0, kPScaleLog2));
     if (ds.n == 0) {
       cuda_check(cudaMemsetAsync(d_gslots_, 0, need * sizeof(SumPair), stream_), "cudaMemsetAsync");

@@ -103,6 +103,10 @@ class Engine {
   void grad_finish(const double* thetas, int P, const double* slot_sums, double n_events,
                    double* values, double* grads);
 
+  // Sizes the device buffers for launches of up to P_nll likelihood points and P_grad
+  // gradient points on `ds` (fits call it before their clock starts).
+  void reserve(const DeviceDataset& ds, int P_nll, int P_grad);
+
   // Current gradient layout (recompiled when parameters change constness).
   const GradPlan& grad_plan();
   bool last_grad_jit() const { return last_grad_jit_ != 0; }
@@ -139,6 +143,7 @@ class Engine {
                     cudaEvent_t ea, cudaEvent_t eb);
   std::string launch_signature(const DeviceDataset& ds, int P, const LaunchChoice& c, const double* h_rows) const;
   void drop_graph();
+  void ensure_gslots(std::size_t need);  // gradient slot buffers (device + pinned host)
   void bind_columns(const HostPlan& plan, const DeviceDataset& ds, ColPtrs& cols) const;
   void ensure(int device, int P, std::size_t scratch);
   const double* upload_constants(const HostPlan& plan, const double* thetas, int P, cudaStream_t s,

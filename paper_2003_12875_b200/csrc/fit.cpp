@@ -192,7 +192,17 @@ void validate(const Model& m, const FitOptions& o, const std::vector<int>& free_
 
 }  // namespace
 
+// Device buffers sized once for the largest launch a fit of d free parameters issues (the
+// batched Hessian: 1 + 2d + 2d(d-1) points; analytic: 2d gradient points), before the
+// fit's clock starts: a buffer growth mid-fit re-pins host memory and frees device memory
+// (an implicit device synchronisation) at an unpredictable cost.
+static void reserve_for_fit(Model& m, Engine& e, const DeviceDataset& ds, bool analytic) {
+  const int d = static_cast<int>(m.free_parameters().size());
+  e.reserve(ds, std::min(1 + 2 * d + 2 * d * std::max(d - 1, 0), 512), analytic ? 2 * d : 0);
+}
+
 FitResult fit_nelder_mead(Model& m, Engine& e, const DeviceDataset& ds, const FitOptions& o) {
+  reserve_for_fit(m, e, ds, false);
   const auto t0 = std::chrono::steady_clock::now();
   BatchObjective f{m, e, ds, m.free_parameters()};
   validate(m, o, f.free_ids);
@@ -358,6 +368,7 @@ struct GradObjective {
 static double resolution(double f) { return 4.0 * std::numeric_limits<double>::epsilon() * std::fabs(f); }
 
 FitResult fit_gradient(Model& m, Engine& e, const DeviceDataset& ds, const FitOptions& o) {
+  reserve_for_fit(m, e, ds, o.analytic_gradient && e.grad_plan().ok);
   const auto t0 = std::chrono::steady_clock::now();
   BatchObjective f{m, e, ds, m.free_parameters()};
   validate(m, o, f.free_ids);

@@ -1113,8 +1113,9 @@ std::string plan_spec_struct(const DevPlan& d) {
     << (d.nderived > 0 ? d.nderived : 1) << "] = {";
   for (int i = 0; i < d.nderived; ++i) {
     const DevDerive& v = d.dv[i];
-    o << (i ? ", " : "") << "{" << v.col << ", " << v.coff << ", " << v.kind << ", " << v.order << ", " << v.dst << ", "
-      << v.row << "}";
+    // (the source row stays launch data, DevPlan::dv: not part of the build)
+    o << (i ? ", " : "") << "{" << v.col << ", " << v.coff << ", " << v.kind << ", " << v.order << ", " << v.dst
+      << ", 0}";
   }
   if (d.nderived == 0) o << "{0, 0, 0, 0, 0, 0}";
   o << "};\n};\n}  // namespace ffb\n";
