@@ -250,6 +250,9 @@ def run_ours(args, w):
     if coll:
         dist.barrier()
     launches = fb.kernel_launches() - launches0
+    build = {0: "static build", 1: "formula-specialised NVRTC build",
+             2: "plan-specialised NVRTC build"}.get(fb.last_launch_jit(model), "?")
+    cached_terms = fb.last_launch_cached(model)
     kms, kcount = fb.kernel_timer_read()
     fb.kernel_timer(False)
     clk = clocks.stop()
@@ -336,7 +339,9 @@ def run_ours(args, w):
         "achieved": achieved, "peak": peak, "frac": achieved / peak,
         "peak_source": "measured live: DFMA-chain microbenchmark (ffcu_fp64_peak); MEASURED_PEAKS.json has no FP64 figure",
         "work_per_event_point": w.fp64_instr_per_event_point,
-        "kernel": "nll_kernel<256,8>", "kernel_ms_avg": avg_kernel_ms, "kernel_launches_timed": kcount,
+        "kernel": f"nll_kernel<256,8> ({build}"
+                  + (f", {cached_terms} launch-constant cached term(s)" if cached_terms else "") + ")",
+        "kernel_ms_avg": avg_kernel_ms, "kernel_launches_timed": kcount,
         "kernel_share_of_step": avg_kernel_ms / (total_ms / args.steps),
         "hbm_algorithmic_bytes_per_launch": n * w.bytes_per_event,
         "hbm_achieved_gbs": n * w.bytes_per_event * info["nchunks"] / (avg_kernel_ms / 1e3) / 1e9,
