@@ -162,6 +162,12 @@ int ffcu_nll_points_partial(ffit_model* m, const ffit_dataset* ds, const double*
 int ffcu_nll_points_device(ffit_model* m, const ffit_dataset* ds, const double* points, int P,
                            double* d_sc, unsigned long long* d_bad, void* stream,
                            unsigned long long* n_evaluations);
+/* The same with the constant rows copied on `upload_stream` (a pipeline's copy stream, next
+ * to its input uploads; the launch on `stream` waits for them): a caller can queue the next
+ * step while the current one runs without its H2D copies queueing behind the kernels. */
+int ffcu_nll_points_device_upload(ffit_model* m, const ffit_dataset* ds, const double* points, int P,
+                                  double* d_sc, unsigned long long* d_bad, void* stream, void* upload_stream,
+                                  unsigned long long* n_evaluations);
 /* NLL and its analytic gradient in ONE fused pass over the events (SURVEY.md
  * §8(f) f1; replaces the finite-difference gradients a Minuit-style driver builds
  * from 2d+1 proj/src/eval.cpp:119-163 evaluations).  grads: P x param_count,

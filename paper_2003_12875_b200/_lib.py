@@ -71,6 +71,7 @@ SIGNATURES = {
     "ffcu_nll_points": (I, [VP, VP, DP, I, DP, LLP, ULLP]),
     "ffcu_nll_points_partial": (I, [VP, VP, DP, I, DP, LLP, ULLP]),
     "ffcu_nll_points_device": (I, [VP, VP, DP, I, VP, VP, VP, ULLP]),
+    "ffcu_nll_points_device_upload": (I, [VP, VP, DP, I, VP, VP, VP, VP, ULLP]),
     "ffcu_nll_grad": (I, [VP, VP, DP, I, DP, DP, LLP, ULLP]),
     "ffcu_grad_slot_count": (I, [VP, IP]),
     "ffcu_nll_grad_partial": (I, [VP, VP, DP, I, DP, LLP, ULLP]),

@@ -416,6 +416,22 @@ FFB_API int ffcu_nll_points_device(ffit_model* m, const ffit_dataset* ds, const 
   });
 }
 
+FFB_API int ffcu_nll_points_device_upload(ffit_model* m, const ffit_dataset* ds, const double* points, int P,
+                                          double* d_sc, unsigned long long* d_bad, void* stream, void* upload_stream,
+                                          unsigned long long* n_evaluations) {
+  return guarded([&] {
+    require(m, "model");
+    require(ds, "dataset");
+    require(points, "points");
+    require(d_sc, "d_sc");
+    require(d_bad, "d_bad");
+    const int k = engine(m).nll_points_device(*ds->d, points, P, reinterpret_cast<ffb::SumPair*>(d_sc), d_bad,
+                                              static_cast<cudaStream_t>(stream),
+                                              static_cast<cudaStream_t>(upload_stream));
+    if (n_evaluations) *n_evaluations = static_cast<unsigned long long>(k);
+  });
+}
+
 FFB_API int ffcu_grad_slot_count(ffit_model* m, int* nslots) {
   return guarded([&] {
     require(m, "model");

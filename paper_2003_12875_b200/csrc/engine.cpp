@@ -186,6 +186,7 @@ Engine::~Engine() {
       cudaFree(d_consts_[k]);
       cudaFreeHost(h_consts_[k]);
       if (staged_[k]) cudaEventDestroy(staged_[k]);
+      if (consumed_[k]) cudaEventDestroy(consumed_[k]);
     }
     cudaFree(d_scratch_);
     cudaFree(d_pairs_);
@@ -212,6 +213,7 @@ void Engine::ensure(int device, int P, std::size_t scratch) {
     cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
     for (int k = 0; k < 2; ++k) {
       cuda_check(cudaEventCreateWithFlags(&staged_[k], cudaEventDisableTiming), "cudaEventCreate");
+      cuda_check(cudaEventCreateWithFlags(&consumed_[k], cudaEventDisableTiming), "cudaEventCreate");
     }
     if (!plan_.programs.empty()) {  // Expression programs: once per engine and device
       const std::size_t bytes = plan_.programs.size() * sizeof(ExprInstr);
@@ -270,6 +272,8 @@ const double* Engine::upload_constants(const HostPlan& plan, const double* theta
 }
 
 const double* Engine::copy_rows(const HostPlan& plan, int k, int P, cudaStream_t s) {
+  // the launch that last read this slot's device rows may run on another stream
+  cuda_check(cudaStreamWaitEvent(s, consumed_[k], 0), "cudaStreamWaitEvent");
   cuda_check(cudaMemcpyAsync(d_consts_[k], h_consts_[k],
                              static_cast<std::size_t>(P) * plan.dev.stride * sizeof(double),
                              cudaMemcpyHostToDevice, s),
@@ -304,7 +308,8 @@ int Engine::build_rows(const HostPlan& plan, const double* thetas, int P, double
 }
 
 int Engine::nll_points_device(const DeviceDataset& ds, const double* thetas, int P,
-                              SumPair* d_pairs, unsigned long long* d_bad, cudaStream_t stream) {
+                              SumPair* d_pairs, unsigned long long* d_bad, cudaStream_t stream,
+                              cudaStream_t upload_stream) {
   if (P <= 0) return 0;
   if (P > kMaxPointsPerLaunch) usage_error("nll_points_device: at most 512 points per call");
   DeviceGuard g(ds.device);
@@ -323,7 +328,15 @@ int Engine::nll_points_device(const DeviceDataset& ds, const double* thetas, int
   // (launch-constant caches may flag rows) come between building the rows and their copy
   const int slot = build_rows(plan_, thetas, P, std::ldexp(1.0, kPScaleLog2));
   const LaunchChoice choice = choose_launch(h_consts_[slot], P, ds.n);
-  const double* d_consts = copy_rows(plan_, slot, P, s);
+  const double* d_consts = nullptr;
+  if (upload_stream && upload_stream != s) {
+    // the rows' copy on the caller's upload stream (beside its input copies: no copy-engine
+    // queueing behind this stream's running kernels), the launch after it
+    d_consts = copy_rows(plan_, slot, P, upload_stream);
+    cuda_check(cudaStreamWaitEvent(s, staged_[slot], 0), "cudaStreamWaitEvent");
+  } else {
+    d_consts = copy_rows(plan_, slot, P, s);
+  }
   cudaEvent_t ea = nullptr, eb = nullptr;
   {
     std::lock_guard<std::mutex> lk(g_timer_mu);
@@ -334,6 +347,7 @@ int Engine::nll_points_device(const DeviceDataset& ds, const double* thetas, int
     }
   }
   const int launches = launch_device(ds, P, d_consts, h_consts_[slot], choice, d_pairs, d_bad, s, ea, eb);
+  cuda_check(cudaEventRecord(consumed_[slot], s), "cudaEventRecord");
   if (s != stream_) {
     cudaEvent_t ev;
     cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");

@@ -90,8 +90,9 @@ class Engine {
   // Asynchronous on `stream`: results stay on the device (d_pairs: P pairs,
   // d_bad: P indices, kNoInvalid if none).  Host-side constant building and the
   // constant upload are part of the call.  Returns kernels launched.
+  // upload_stream (optional): where the constant rows are copied (a caller's copy stream).
   int nll_points_device(const DeviceDataset& ds, const double* thetas, int P, SumPair* d_pairs,
-                        unsigned long long* d_bad, cudaStream_t stream);
+                        unsigned long long* d_bad, cudaStream_t stream, cudaStream_t upload_stream = nullptr);
 
   // Analytic gradient in the same pass over the events (plan.hpp DevGradPlan):
   // P points, one launch pair per <= 512 points.  Throws Usage when the model's
@@ -160,6 +161,7 @@ class Engine {
   double* d_consts_[2] = {nullptr, nullptr};
   double* h_consts_[2] = {nullptr, nullptr};  // pinned
   cudaEvent_t staged_[2] = {nullptr, nullptr};
+  cudaEvent_t consumed_[2] = {nullptr, nullptr};  // the last launch reading slot k's device rows
   int slot_ = 0;
   void* d_scratch_ = nullptr;
   SumPair* d_pairs_ = nullptr;

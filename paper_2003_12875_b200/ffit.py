@@ -360,13 +360,20 @@ def nll_points_partial(model: Model, ds: DataSet, points):
     return sc, bad
 
 
-def nll_points_device(model: Model, ds: DataSet, points, d_sc_ptr, d_bad_ptr, stream_ptr=None):
-    """Async multi-point NLL into device buffers (2P doubles, P uint64) on a CUDA stream."""
+def nll_points_device(model: Model, ds: DataSet, points, d_sc_ptr, d_bad_ptr, stream_ptr=None,
+                      upload_stream_ptr=None):
+    """Async multi-point NLL into device buffers (2P doubles, P uint64) on a CUDA stream;
+    upload_stream_ptr: copy the constant rows on that stream instead (a pipeline's copy stream)."""
     pts = _f64(np.atleast_2d(points))
     ne = ctypes.c_ulonglong()
-    _check(lib().ffcu_nll_points_device(model.handle, ds.handle, _dp(pts), pts.shape[0],
-                                        VP(d_sc_ptr), VP(d_bad_ptr), VP(stream_ptr or 0),
-                                        ctypes.byref(ne)))
+    if upload_stream_ptr:
+        _check(lib().ffcu_nll_points_device_upload(model.handle, ds.handle, _dp(pts), pts.shape[0],
+                                                   VP(d_sc_ptr), VP(d_bad_ptr), VP(stream_ptr or 0),
+                                                   VP(upload_stream_ptr), ctypes.byref(ne)))
+    else:
+        _check(lib().ffcu_nll_points_device(model.handle, ds.handle, _dp(pts), pts.shape[0],
+                                            VP(d_sc_ptr), VP(d_bad_ptr), VP(stream_ptr or 0),
+                                            ctypes.byref(ne)))
     return ne.value
 
 
