@@ -1,0 +1,106 @@
+"""Randomised parity sweep: seeded random models (mixtures of every leaf kind, products over
+two observables), random launch shapes (few points: streaming kernels / graph replay; many
+points: tile kernels, static and plan-specialised, with and without launch-constant caches)
+against the oracle's compensated NLL at 1e-12.  Data are uniform over the observable ranges
+(the NLL does not need the events to follow the pdf)."""
+import numpy as np
+import pytest
+
+import paper_2003_12875_b200 as fb
+from oracle.oracle import OracleModel
+
+pytestmark = pytest.mark.gpu
+
+NLL_TOL = 1e-12
+LO, HI = 0.5, 5.0
+
+
+def leaf(rng, name, obs, params):
+    """One random leaf on [LO, HI]: its model lines and pdf call."""
+    kind = rng.choice(["Gaussian", "Exponential", "Chebychev", "Polynomial", "ArgusBG", "ChiSquare",
+                       "JohnsonSU"])
+    def par(p, v, lo, hi, const=False):
+        params.append(f"parameter {p} {v!r} {lo!r} {hi!r}" + (" const" if const else ""))
+        return p
+    if kind == "Gaussian":
+        args = [par(f"{name}_m", float(rng.uniform(1, 4.5)), 0.0, 6.0),
+                par(f"{name}_s", float(rng.uniform(0.3, 1.5)), 0.05, 5.0)]
+    elif kind == "Exponential":
+        args = [par(f"{name}_c", float(rng.uniform(-0.8, 0.2)), -3.0, 1.0)]
+    elif kind == "Chebychev":
+        args = [par(f"{name}_a{k}", float(rng.uniform(-0.15, 0.15)), -1.0, 1.0) for k in range(1, 4)]
+    elif kind == "Polynomial":
+        args = [par(f"{name}_a{k}", float(rng.uniform(0.01, 0.2)), 0.0, 1.0) for k in range(1, 3)]
+    elif kind == "ArgusBG":
+        args = [par(f"{name}_m0", 5.6, 5.2, 6.0, const=True), par(f"{name}_c", float(rng.uniform(-8, -1)), -20.0, 0.0),
+                par(f"{name}_p", 0.5, 0.1, 2.0, const=True)]
+    elif kind == "ChiSquare":
+        args = [par(f"{name}_k", float(rng.uniform(2.5, 6.0)), 1.0, 20.0)]
+    else:
+        args = [par(f"{name}_mu", float(rng.uniform(1.5, 3.5)), 0.0, 6.0),
+                par(f"{name}_l", float(rng.uniform(0.5, 1.5)), 0.1, 3.0),
+                par(f"{name}_g", float(rng.uniform(-0.5, 0.5)), -3.0, 3.0),
+                par(f"{name}_d", float(rng.uniform(0.8, 1.6)), 0.1, 3.0)]
+    return f"pdf {name} {kind}({obs}, {', '.join(args)})"
+
+
+def mixture(rng, tag, obs, params, pdfs):
+    k = int(rng.integers(1, 4))
+    names = []
+    for i in range(k):
+        n = f"{tag}{i}"
+        pdfs.append(leaf(rng, n, obs, params))
+        names.append(n)
+    if k == 1:
+        return names[0]
+    args = []
+    for i, n in enumerate(names):
+        args.append(n)
+        if i < k - 1:
+            f = f"{tag}_f{i}"
+            params.append(f"parameter {f} {float(rng.uniform(0.15, 0.3))!r} 0.0 1.0")
+            args.append(f)
+    pdfs.append(f"pdf {tag}mix AddPdf({', '.join(args)})")
+    return f"{tag}mix"
+
+
+def random_model(seed):
+    rng = np.random.default_rng(seed)
+    params, pdfs = [], []
+    two = seed % 3 == 0  # every third model a product over two observables
+    lines = [f"observable x {LO} {HI}"] + ([f"observable y {LO} {HI}"] if two else [])
+    a = mixture(rng, "a", "x", params, pdfs)
+    if two:
+        b = mixture(rng, "b", "y", params, pdfs)
+        pdfs.append(f"pdf model ProdPdf({a}, {b})")
+    return "\n".join(lines + params + pdfs) + "\n"
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_model_parity(seed):
+    text = random_model(seed)
+    m = fb.Model.from_string(text)
+    o = OracleModel(text)
+    rng = np.random.default_rng(1000 + seed)
+    n = int(rng.choice([2049, 30_001, 100_003]))
+    cols = {obs: rng.uniform(LO, HI, n) for obs in m.observables}
+    ds = fb.DataSet.from_columns(cols)
+    xs = [cols[k] for k in m.observables]
+    base = m.theta()
+    free = [k for k, nm in enumerate(m.param_names) if not m.is_constant(nm)]
+    for P, moving in ((1, free), (3, free), (12, free), (40, free[:1]), (16, free[-1:])):
+        pts = np.tile(base, (P, 1))
+        for p in range(P):
+            for k in moving:
+                pts[p, k] = base[k] * (1.0 + 1e-3 * (p + 1) / P)
+        for spec in (False, True):
+            old = fb.plan_spec_min_work(0 if spec else -1)
+            try:
+                vals, bad, _ = fb.nll_points(m, ds, pts)
+            finally:
+                fb.plan_spec_min_work(old)
+            for p in sorted({0, P - 1}):
+                _, comp, ob = o.nll(xs, pts[p])
+                assert bad[p] == ob, (text, P, spec, p)
+                if ob < 0:
+                    assert abs(vals[p] - comp) <= NLL_TOL * abs(comp), (text, P, spec, p, vals[p], comp)
