@@ -942,3 +942,26 @@ def test_launch_constant_cache_partly_shared_m0():
         _, comp, ob = o.nll(cols, pts[p])
         assert bad[p] == ob == -1
         assert abs(hybrid[p] - comp) <= NLL_TOL * abs(comp)
+
+
+def test_more_points_than_one_launch():
+    """P > 512 (the per-launch cap) is split into several launches; every chunk boundary
+    point matches the oracle and is bit-identical to the same point evaluated in a launch
+    of the same kernel shape."""
+    m, ds, xs, o = setup(ARGUS_OURS, 30_001, 77)
+    base = m.theta()
+    P = 1100
+    pts = np.tile(base, (P, 1))
+    free = [k for k, nm in enumerate(m.param_names) if not m.is_constant(nm)]
+    for p in range(P):
+        for k in free:
+            pts[p, k] = base[k] * (1.0 + 1e-4 * np.sin(p + k))
+    vals, bad, _ = fb.nll_points(m, ds, pts)
+    assert len(vals) == P and np.all(np.asarray(bad) == -1)
+    for p in (0, 511, 512, 1023, 1024, P - 1):
+        _, comp, ob = o.nll(xs, pts[p])
+        assert ob == -1
+        assert abs(vals[p] - comp) <= NLL_TOL * abs(comp), (p, vals[p], comp)
+    # the second chunk alone (512 points: the same kernel shape as inside the big call)
+    v2, _, _ = fb.nll_points(m, ds, pts[512:1024])
+    assert np.array_equal(np.asarray(v2), np.asarray(vals[512:1024]))
