@@ -125,6 +125,7 @@ int ffcu_dataset_copy_from_host(ffit_dataset* ds, const double* const* cols);
 int ffcu_dataset_copy_from_host_async(ffit_dataset* ds, const double* const* cols, void* stream);
 /* Rows [begin, end) as a zero-copy view (event sharding). */
 int ffcu_dataset_slice(const ffit_dataset* ds, long long begin, long long end, ffit_dataset** out);
+/* Columns: count, names, a column copied to host memory, a column's device pointer. */
 int ffcu_dataset_ncols(const ffit_dataset* ds);
 const char* ffcu_dataset_column_name(const ffit_dataset* ds, int i);
 int ffcu_dataset_download(const ffit_dataset* ds, int col, double* host_out);
@@ -248,6 +249,7 @@ double ffcu_plan_spec_min_work(double v);
  * the model's last gradient launch ran it. */
 int ffcu_grad_spec_source(ffit_model* m, int compile_ks, char* buf, int cap);
 int ffcu_last_grad_jit(ffit_model* m);
+/* Model introspection: the named pdfs and the observables, in model-file order. */
 int ffcu_model_pdf_count(const ffit_model* m);
 const char* ffcu_model_pdf_name(const ffit_model* m, int i);
 int ffcu_model_observable_count(const ffit_model* m);
@@ -266,9 +268,11 @@ int ffcu_fit_gradient_opts(ffit_model* m, const ffit_dataset* ds, double toleran
                            long max_iterations, int analytic, ffit_fit_result** out);
 /* 1 if the fit's gradients came from the fused pass. */
 int ffcu_result_analytic_gradient(const ffit_fit_result* r);
+/* fit_gradient: BFGS iterations taken. */
 int ffcu_result_iterations(const ffit_fit_result* r);
 /* fit_gradient: the last estimated distance to the minimum, g^T H^-1 g / 2. */
 double ffcu_result_edm(const ffit_fit_result* r);
+/* fit_gradient: likelihood / gradient launches, and the per-iteration NLL trace. */
 unsigned long long ffcu_result_launches(const ffit_fit_result* r);
 int ffcu_result_trace(const ffit_fit_result* r, double* out, int cap);
 
