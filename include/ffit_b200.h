@@ -38,8 +38,10 @@ enum {
 };
 
 /* Evaluation modes -- reference include/ffit.h:27-31, plus FFIT_MODE_GPU.
- * BATCH_PRECISE, BATCH_FAST and GPU all run the fused sm_100a kernel;
- * SCALAR (the reference's per-entry graph walk) is rejected with FFIT_ERR_USAGE. */
+ * Every mode runs the fused sm_100a kernel.  The reference's SCALAR is bitwise equal
+ * to its BATCH_PRECISE (proj/tests/test_eval.cpp:113-157), and here SCALAR, BATCH_PRECISE,
+ * BATCH_FAST and GPU return the same bits, so the reference CLI's mode comparisons
+ * (tools/ffit_main.cpp bench / parity) relink unchanged. */
 typedef enum {
   FFIT_MODE_SCALAR = 0,
   FFIT_MODE_BATCH_PRECISE = 1,

@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <charconv>
 #include <fstream>
 #include <limits>
 #include <memory>
@@ -54,15 +55,18 @@ void require(const void* p, const char* what) {
   if (!p) ffb::usage_error(std::string(what) + " must not be null");
 }
 
+// Every reference mode runs the fused sm_100a kernel.  The reference defines Scalar as
+// bitwise equal to BatchPrecise (proj/src/eval.cpp:96-117 vs 119-163, pinned by
+// proj/tests/test_eval.cpp:113-157), so FFIT_MODE_SCALAR returns the GPU's Precise result
+// bit for bit; the reference CLI's `bench` / `parity` (proj/tools/ffit_main.cpp:177,
+// 188-189, 216-217) compare Scalar against the batch modes and find 0 deviation.
 void require_gpu_mode(ffit_mode mode) {
   switch (mode) {
+    case FFIT_MODE_SCALAR:
     case FFIT_MODE_BATCH_PRECISE:
     case FFIT_MODE_BATCH_FAST:
     case FFIT_MODE_GPU:
       return;
-    case FFIT_MODE_SCALAR:
-      ffb::usage_error("scalar (per-entry graph walk) mode is the CPU reference's; this library "
-                       "evaluates on the GPU (use FFIT_MODE_GPU)");
   }
   ffb::usage_error("unknown evaluation mode");
 }
@@ -84,24 +88,37 @@ std::unique_ptr<ffit_model> make_model(std::unique_ptr<ffb::Model> mm) {
   return m;
 }
 
+// CSV cells exactly as the reference reads them (proj/src/dataset.cpp:11-45): split on
+// ',', trailing ' ' / '\r' and leading ' ' trimmed (tabs are kept), each cell parsed by
+// std::from_chars over the whole cell (locale-independent; no leading '+', no hex).
 std::vector<std::string> split_csv(const std::string& line) {
   std::vector<std::string> out;
-  std::string cur;
-  for (const char ch : line) {
-    if (ch == ',') {
-      out.push_back(cur);
-      cur.clear();
-    } else if (ch != '\r') {
-      cur += ch;
-    }
+  std::size_t start = 0;
+  while (true) {
+    const std::size_t comma = line.find(',', start);
+    out.push_back(line.substr(start, comma == std::string::npos ? std::string::npos : comma - start));
+    if (comma == std::string::npos) break;
+    start = comma + 1;
   }
-  out.push_back(cur);
-  for (auto& s : out) {
-    const auto b = s.find_first_not_of(" \t");
-    const auto e = s.find_last_not_of(" \t");
-    s = b == std::string::npos ? std::string() : s.substr(b, e - b + 1);
+  for (auto& f : out) {
+    while (!f.empty() && (f.back() == '\r' || f.back() == ' ')) f.pop_back();
+    std::size_t i = 0;
+    while (i < f.size() && f[i] == ' ') ++i;
+    f.erase(0, i);
   }
   return out;
+}
+
+double parse_cell(const std::string& cell, std::size_t row, const std::string& col) {
+  double v = 0.0;
+  const char* first = cell.data();
+  const char* last = first + cell.size();
+  const auto [ptr, ec] = std::from_chars(first, last, v);
+  if (ec != std::errc() || ptr != last) {
+    ffb::data_error("unparsable numeric cell at row " + std::to_string(row) + ", column '" + col + "': '" + cell +
+                    "'");
+  }
+  return v;
 }
 
 }  // namespace
@@ -227,13 +244,7 @@ FFB_API int ffit_dataset_read_csv(const ffit_model* m, const char* path, ffit_da
       }
       bool in_range = true;
       for (std::size_t s = 0; s < obs.size(); ++s) {
-        const std::string& cell = f[idx[s]];
-        char* end = nullptr;
-        const double v = std::strtod(cell.c_str(), &end);
-        if (cell.empty() || end != cell.c_str() + cell.size()) {
-          ffb::data_error("bad number at row " + std::to_string(row) + ", column '" + obs[s].name +
-                          "': '" + cell + "'");
-        }
+        const double v = parse_cell(f[idx[s]], row, obs[s].name);
         parsed[s] = v;
         if (!(v >= obs[s].lo && v <= obs[s].hi)) in_range = false;
       }

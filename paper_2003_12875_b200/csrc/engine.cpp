@@ -271,6 +271,12 @@ const double* Engine::upload_constants(const HostPlan& plan, const double* theta
   return copy_rows(plan, k, P, s);
 }
 
+// Every launch that reads slot k's device rows records consumed_[k] on its stream right
+// after it is queued; copy_rows makes the next copy into that slot wait for it.
+void Engine::mark_consumed(int k, cudaStream_t s) {
+  cuda_check(cudaEventRecord(consumed_[k], s), "cudaEventRecord");
+}
+
 const double* Engine::copy_rows(const HostPlan& plan, int k, int P, cudaStream_t s) {
   // the launch that last read this slot's device rows may run on another stream
   cuda_check(cudaStreamWaitEvent(s, consumed_[k], 0), "cudaStreamWaitEvent");
@@ -347,7 +353,7 @@ int Engine::nll_points_device(const DeviceDataset& ds, const double* thetas, int
     }
   }
   const int launches = launch_device(ds, P, d_consts, h_consts_[slot], choice, d_pairs, d_bad, s, ea, eb);
-  cuda_check(cudaEventRecord(consumed_[slot], s), "cudaEventRecord");
+  mark_consumed(slot, s);
   if (s != stream_) {
     cudaEvent_t ev;
     cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
@@ -660,6 +666,7 @@ NllGradResult Engine::nll_grad_points(const DeviceDataset& ds, const double* the
                                  ks, ea, eb);
       last_grad_jit_ = li.jit;
       cuda_check(cudaGetLastError(), "launch_nll_grad");
+      mark_consumed(slot_, stream_);
       r.launches += li.launches;
       count_launches(li.launches);
     }
@@ -719,8 +726,10 @@ void Engine::eval_batch(int pdf, const DeviceDataset& ds, const double* theta, d
   if (!out_on_device) {
     cuda_check(cudaMalloc(&d_out, static_cast<std::size_t>(ds.n) * sizeof(double)), "cudaMalloc(out)");
   }
+  const int slot = slot_;  // upload_constants filled this slot
   count_launches(launch_eval(plan.dev, cols, ds.n, d_consts, d_out, s));
   cuda_check(cudaGetLastError(), "launch_eval");
+  mark_consumed(slot, s);  // a later copy into this slot (any stream) waits for the kernel
   if (!out_on_device) {
     cuda_check(cudaMemcpyAsync(out, d_out, static_cast<std::size_t>(ds.n) * sizeof(double),
                                cudaMemcpyDeviceToHost, s),

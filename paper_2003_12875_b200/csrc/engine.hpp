@@ -139,6 +139,7 @@ class Engine {
   LaunchChoice choose_launch(double* h_rows, int P, long long n);
   int build_rows(const HostPlan& plan, const double* thetas, int P, double extra_scale);  // -> slot
   const double* copy_rows(const HostPlan& plan, int slot, int P, cudaStream_t s);
+  void mark_consumed(int slot, cudaStream_t s);
   int launch_device(const DeviceDataset& ds, int P, const double* d_consts, const double* h_rows,
                     const LaunchChoice& c, SumPair* d_pairs, unsigned long long* d_bad, cudaStream_t s,
                     cudaEvent_t ea, cudaEvent_t eb);

@@ -172,15 +172,38 @@ class DataSet:
         return cls(h)
 
     @classmethod
-    def from_device(cls, columns: dict, device: int = 0) -> "DataSet":
-        """Zero-copy view over device tensors (anything with data_ptr())."""
+    def from_device(cls, columns: dict, device: int | None = None) -> "DataSet":
+        """Zero-copy view over device tensors (torch tensors: anything with data_ptr(),
+        dtype, device, numel() and is_contiguous()).  Every column must be a contiguous
+        float64 CUDA tensor of the same length, all on one device (the view's device;
+        `device`, if given, must agree) -- the kernels read n doubles from each pointer."""
         names = list(columns)
         tensors = [columns[n] for n in names]
-        n = int(tensors[0].numel()) if tensors else 0
+        if not tensors:
+            raise FfitError(USAGE, "from_device needs at least one column")
+        n = int(tensors[0].numel())
+        devs = set()
+        for name, t in zip(names, tensors):
+            dt = str(getattr(t, "dtype", ""))
+            if dt not in ("torch.float64", "float64"):
+                raise FfitError(USAGE, f"column {name!r}: dtype {dt or type(t).__name__}, expected float64")
+            dev = getattr(t, "device", None)
+            if dev is None or getattr(dev, "type", None) != "cuda":
+                raise FfitError(USAGE, f"column {name!r} is not on a CUDA device ({dev})")
+            if not t.is_contiguous():
+                raise FfitError(USAGE, f"column {name!r} is not contiguous (a strided view?)")
+            if int(t.numel()) != n:
+                raise FfitError(USAGE, f"column {name!r} has {int(t.numel())} rows, expected {n}")
+            devs.add(dev.index if dev.index is not None else 0)
+        if len(devs) != 1:
+            raise FfitError(USAGE, f"columns span several devices: {sorted(devs)}")
+        tdev = devs.pop()
+        if device is not None and int(device) != tdev:
+            raise FfitError(USAGE, f"device={device} but the columns live on cuda:{tdev}")
         cn = (CP * len(names))(*[s.encode() for s in names])
         cp = (VP * len(names))(*[t.data_ptr() for t in tensors])
         h = VP()
-        _check(lib().ffcu_dataset_from_device(cn, cp, len(names), n, device, ctypes.byref(h)))
+        _check(lib().ffcu_dataset_from_device(cn, cp, len(names), n, tdev, ctypes.byref(h)))
         return cls(h, keep=tensors)
 
     @classmethod
@@ -273,11 +296,10 @@ class NllValue:
 def nll(model: Model, ds: DataSet, mode: EvalMode = EvalMode.Gpu) -> NllValue:
     """Reference ffit::nll (proj/src/eval.cpp:165-172) on the GPU.
 
+    Every mode runs the fused kernel (Scalar == BatchPrecise bitwise, as in the reference);
     first_invalid comes from the multi-point entry (same launch)."""
-    v = ctypes.c_double()
-    ne = ctypes.c_ulonglong()
-    if int(mode) == EvalMode.Scalar:
-        _check(lib().ffit_nll(model.handle, ds.handle, int(mode), ctypes.byref(v), ctypes.byref(ne)))
+    if int(mode) not in tuple(EvalMode):
+        raise FfitError(1, "unknown evaluation mode")
     vals, bad, launches = nll_points(model, ds, model.theta()[None, :])
     return NllValue(float(vals[0]), ds.n_rows, int(launches), int(bad[0]))
 

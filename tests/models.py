@@ -179,3 +179,101 @@ FIT_CASES = {
                       data_from="oracle", start={"m": 5.2785, "s": 0.0032, "c": -18.0, "f": 0.12},
                       free=["m", "s", "c", "f"]),
 }
+
+
+# ---------------------------------------------------------------------------
+# exp at the edges of its range (tests/golden/make_edge_golden.py):
+# densities in glibc's gradual-underflow window (exp argument in (-745.13, -707]) are
+# SUBNORMAL and valid in the reference, below it they are 0 and the event is invalid
+# (proj/src/eval.cpp:138-145); exp(c x) stays finite up to c x = 709.78.
+
+GAUSS_WIDE = """
+observable x -50 50
+parameter mu 0 -1 1
+parameter sigma 1 0.5 2
+pdf g Gaussian(x, mu, sigma)
+"""
+
+FAR_MIX = """
+observable x -60 60
+parameter m1 -5 -10 10
+parameter s1 1 0.5 2
+parameter m2 5 -10 10
+parameter s2 1 0.5 2
+parameter f 0.4 0 1
+pdf a Gaussian(x, m1, s1)
+pdf b Gaussian(x, m2, s2)
+pdf model WeightedSum(a, f, b)
+"""
+
+EXPO_EDGE = """
+observable x 700 709.7
+parameter c 1.0 0.5 1.0
+pdf e Exponential(x, c)
+"""
+
+
+def edge_data(sub_at, zero_at, n=4099):
+    """Standard-normal events, one at exponent -720 (subnormal p), one at -800 (p = 0) and
+    one more at -900 later on; zero_at = None leaves only the subnormal one."""
+    import math
+
+    import numpy as np
+    x = np.random.default_rng(5).normal(0.0, 1.0, n)
+    x[sub_at] = math.sqrt(2.0 * 720.0)
+    if zero_at is not None:
+        x[zero_at] = -math.sqrt(2.0 * 800.0)
+        x[3000] = math.sqrt(2.0 * 900.0)
+    return x
+
+
+def far_mix_data():
+    import math
+
+    import numpy as np
+    rng = np.random.default_rng(9)
+    x = np.concatenate([rng.normal(-5, 1, 3000), rng.normal(5, 1, 3000)])
+    x[17] = -5 - math.sqrt(2 * 722.0)   # component a at -722, b far below -745
+    x[1234] = 5 + math.sqrt(2 * 710.0)  # component b at -710 (subnormal), a 0
+    return x
+
+
+def expo_edge_data():
+    import numpy as np
+    x = np.random.default_rng(11).uniform(700.0, 709.7, 30_011)
+    x[:4] = [709.7, 709.65, 707.01, 708.2]
+    return x
+
+
+def c1_sigma720_text(x):
+    """The C1 model with sigma set so that the most distant event's exponent is -720."""
+    import math
+
+    import numpy as np
+    sigma = float(np.max(np.abs(x - 1.0))) / math.sqrt(2.0 * 720.0)
+    return f"""
+observable x -10 10
+parameter mean 1.0 -5 5
+parameter sigma {sigma!r} 0.1 10
+pdf g Gaussian(x, mean, sigma)
+"""
+
+
+EXPR_GAUSS_WIDE = """
+observable x -50 50
+parameter mu 0 -1 1
+parameter sigma 1 0.5 2
+pdf g Expression("exp(-0.5*((x-mu)/sigma)^2)", x, mu, sigma)
+"""
+
+# name -> (text, events) ; c1_sigma720 is built from the reference sampler's C1 events
+EDGE_CASES = {
+    "gauss_sub_then_zero": lambda: (GAUSS_WIDE, edge_data(3, 10)),
+    "gauss_zero_then_sub": lambda: (GAUSS_WIDE, edge_data(10, 3)),
+    "gauss_sub_only": lambda: (GAUSS_WIDE, edge_data(3, None)),
+    "far_mix": lambda: (FAR_MIX, far_mix_data()),
+    "expo_overflow_edge": lambda: (EXPO_EDGE, expo_edge_data()),
+    # the reference's Expression + adaptive-Simpson route (the formula-specialised build)
+    "expr_sub_then_zero": lambda: (EXPR_GAUSS_WIDE, edge_data(3, 10)),
+    "expr_sub_only": lambda: (EXPR_GAUSS_WIDE, edge_data(3, None)),
+}

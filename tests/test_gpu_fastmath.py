@@ -17,7 +17,7 @@ def ulps(a, b):
 
 def test_exp_accuracy_over_the_working_range():
     rng = np.random.default_rng(0)
-    # the kernel's exp is exact-to-2-ulp on |x| <= 707 and saturates beyond (fastmath.cuh)
+    # the kernel's exp is exact-to-2-ulp on |x| <= 707 (the edges: test_exp_range_edges_match_glibc)
     x = np.concatenate([rng.uniform(-707.0, 707.0, 2_000_000), rng.uniform(-1, 1, 500_000),
                         rng.uniform(-40, 0, 500_000), np.array([0.0, -0.0, 1e-300, -1e-300, 1.0, -1.0])])
     got = fb.ffit.math_probe("exp", x)
@@ -26,14 +26,32 @@ def test_exp_accuracy_over_the_working_range():
     assert np.max(np.abs(got - want) / want) <= 4.5e-16
 
 
-def test_exp_saturation():
-    """Beyond |x| = 707 the kernel's exp saturates (0 below, +inf above); NaN / inf
-    arguments are never evaluated: events with non-finite data are flagged invalid by the
-    kernels and non-finite parameters are rejected on the host."""
-    x = np.array([-800.0, -746.0, -707.1, 707.1, 710.0, 800.0, 1e300, -1e300])
+def test_exp_range_edges_match_glibc():
+    """Past |x| = 707 the device exp takes its edge path (fastmath.cuh exp_edge): gradual
+    underflow into the subnormals down to -745.13, +0 below; finite up to 709.78, +inf
+    above; NaN / inf arguments as glibc.  Compared with glibc's exp (math.exp)."""
+    rng = np.random.default_rng(3)
+    x = np.concatenate([rng.uniform(-745.2, -707.0, 200_000), rng.uniform(707.0, 709.78, 50_000),
+                        np.array([-707.0, -707.5, -708.39, -708.4, -710.0, -720.0, -744.0, -745.0,
+                                  -745.13, -745.14, -746.0, -800.0, -1e300, 707.5, 709.0, 709.78])])
     got = fb.ffit.math_probe("exp", x)
-    assert list(got[[0, 1, 2, 7]]) == [0.0, 0.0, 0.0, 0.0]
-    assert np.all(np.isinf(got[[3, 4, 5, 6]]))
+
+    def gexp(v):
+        try:
+            return math.exp(v)
+        except OverflowError:
+            return math.inf
+    want = np.array([gexp(float(v)) for v in x])
+    fin = want > 0
+    # normal results: 2 ulp; subnormal ones: one rounding of a 2-ulp value
+    tol = np.maximum(2.0 * np.spacing(want), 2.0 * 2.0 ** -1074)
+    assert np.all(np.abs(got[fin] - want[fin]) <= tol[fin])
+    assert np.all(got[~fin] == 0.0)
+    sub = (want > 0) & (want < 2.2250738585072014e-308)
+    assert sub.sum() > 50_000 and np.all(got[sub] > 0)
+    edge = fb.ffit.math_probe("exp", np.array([709.79, 710.0, 800.0, 1e300, math.inf, -math.inf, math.nan]))
+    assert np.all(np.isinf(edge[:5])) and np.all(edge[:5] > 0)
+    assert edge[5] == 0.0 and math.isnan(edge[6])
 
 
 def test_log_accuracy_absolute_and_relative():

@@ -439,14 +439,38 @@ def test_c_abi_entry_points():
     assert nev == 2
     v2, _ = fb.nll_c(m, ds, fb.EvalMode.BatchPrecise)
     assert v2 == value
+    # Scalar == BatchPrecise bitwise in the reference (proj/tests/test_eval.cpp:113-157);
+    # every mode returns the fused kernel's bits here, probabilities included
+    for mode in (fb.EvalMode.Scalar, fb.EvalMode.BatchFast):
+        assert fb.nll_c(m, ds, mode)[0] == value
+        assert np.array_equal(fb.probabilities(m, ds, mode), fb.probabilities(m, ds, fb.EvalMode.Gpu))
     with pytest.raises(fb.FfitError) as e:
-        fb.nll_c(m, ds, fb.EvalMode.Scalar)
+        fb.nll_c(m, ds, 7)
     assert e.value.code == 1
     o = OracleModel(MIX)
     x = ds.column("x")
     assert abs(value - o.nll([x])[1]) <= NLL_TOL * abs(value)
     m.set("sigma", 1.5)
     assert fb.nll_c(m, ds)[0] != value
+
+
+@pytest.mark.parametrize("cell,ok", [("1.25", True), ("  1.25 \r", True), ("-3e-1", True), ("+1.25", False),
+                                     ("0x1p0", False), ("\t1.25", False), ("1.25\t", False),
+                                     ("1.25x", False), ("nan", True)])
+def test_csv_cells_parse_as_the_reference(tmp_path, cell, ok):
+    """proj/src/dataset.cpp:11-45: split on ',', trim trailing ' '/'\\r' and leading ' ',
+    std::from_chars over the whole cell; anything else is FFIT_ERR_DATA 'unparsable numeric
+    cell'.  (nan parses, then fails the range check and the row is dropped.)"""
+    m = fb.Model.from_string(MIX)
+    p = tmp_path / "c.csv"
+    p.write_bytes(("x\n0.5\n" + cell + "\n").encode())
+    if ok:
+        ds, dropped = fb.DataSet.read_csv(m, str(p))
+        assert ds.n_rows + dropped == 2
+    else:
+        with pytest.raises(fb.FfitError) as e:
+            fb.DataSet.read_csv(m, str(p))
+        assert e.value.code == 2 and "unparsable numeric cell at row 2, column 'x'" in e.value.message
 
 
 def test_csv_round_trip(tmp_path):

@@ -298,3 +298,46 @@ def test_plan_spec_threshold_switch():
         assert fb.plan_spec_min_work(-2) == -1
     finally:
         fb.plan_spec_min_work(old)
+
+
+def test_from_device_rejects_what_the_kernels_cannot_read():
+    """DataSet.from_device checks dtype, device, contiguity and lengths before the view is
+    made (the kernels read n fp64 values from each pointer)."""
+    import torch
+    good = torch.zeros(16, dtype=torch.float64)
+    cases = {
+        "float32": {"x": torch.zeros(16, dtype=torch.float32)},
+        "host tensor": {"x": good},
+        "no columns": {},
+    }
+    for what, cols in cases.items():
+        with pytest.raises(fb.FfitError) as e:
+            fb.DataSet.from_device(cols)
+        assert e.value.code == fb.ffit.USAGE, what
+
+    class FakeCuda:  # a CUDA tensor's surface, without a GPU
+        def __init__(self, n, dtype="torch.float64", contiguous=True, index=0):
+            self._n, self.dtype, self._c = n, dtype, contiguous
+            self.device = type("D", (), {"type": "cuda", "index": index})()
+
+        def numel(self):
+            return self._n
+
+        def is_contiguous(self):
+            return self._c
+
+        def data_ptr(self):
+            return 256
+
+    bad = {
+        "strided": {"x": FakeCuda(16, contiguous=False)},
+        "ragged": {"x": FakeCuda(16), "y": FakeCuda(15)},
+        "two devices": {"x": FakeCuda(16), "y": FakeCuda(16, index=1)},
+        "float32 cuda": {"x": FakeCuda(16, dtype="torch.float32")},
+    }
+    for what, cols in bad.items():
+        with pytest.raises(fb.FfitError) as e:
+            fb.DataSet.from_device(cols)
+        assert e.value.code == fb.ffit.USAGE, what
+    with pytest.raises(fb.FfitError):
+        fb.DataSet.from_device({"x": FakeCuda(16, index=1)}, device=0)

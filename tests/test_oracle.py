@@ -254,3 +254,31 @@ pdf m WeightedSum(a, f, b)
     _, e, _ = ext.nll(cols)
     _, f, _ = frac.nll(cols)
     assert e == pytest.approx(f + 1000 - 5000 * math.log(1000), rel=1e-13)
+
+
+# ---------------------------------------------------------------- exp range edges
+
+def _edge_cases():
+    g = _npz("edge_models.npz")
+    names = sorted({k.split("/")[0] for k in g.files})
+    return g, names
+
+
+@pytest.mark.parametrize("name", _edge_cases()[1])
+def test_oracle_exp_edges_bit_exact(name):
+    """Densities in glibc's gradual-underflow window (subnormal, valid), below it (0,
+    first_invalid) and exp near overflow: the oracle reproduces the reference's per-event
+    values, both NLL sums and first_invalid bit for bit (tests/golden/make_edge_golden.py)."""
+    g, _ = _edge_cases()
+    text = bytes(g[f"{name}/text"]).decode()
+    if "Expression" in text:
+        pytest.skip("Expression pdfs: the reference's route is the golden itself (GPU test)")
+    x, p, sc = g[f"{name}/x"], g[f"{name}/p"], g[f"{name}/scalars"]
+    o = OracleModel(text)
+    assert np.array_equal(o.probabilities([x]), p)
+    naive, comp, bad = o.nll([x])
+    assert bad == sc[2]
+    assert (naive == sc[0] and comp == sc[1]) or (bad >= 0 and naive == comp == math.inf == sc[0])
+    assert o.normalization() == sc[3]
+    if name != "expo_overflow_edge":
+        assert 0.0 < p[p > 0].min() < 2.2250738585072014e-308  # the case exercises the window
