@@ -191,6 +191,12 @@ int ffcu_nll_grad_finish(ffit_model* m, const double* points, int P, const doubl
                          double n_events, double* values, double* grads);
 /* Fixed-rank-order compensated combine of R x P device pairs into P pairs. */
 int ffcu_combine_pairs_device(const double* d_in, int R, int P, double* d_out, void* stream);
+/* The sharded exchange's combine (csrc/shard.hpp) for callers doing their own collective:
+ * d_in = R gathered rank blocks of 2*rows + P 8-byte words ([rows Neumaier pairs | P local
+ * first-invalid indices]); d_out = rows pairs combined in rank order, d_bad = P global
+ * indices (d_offsets[r] = rank r's first global row; 0xFFFFFFFFFFFFFFFF = none). */
+int ffcu_combine_shards_device(const double* d_in, int R, int rows, int P, const long long* d_offsets,
+                               double* d_out, unsigned long long* d_bad, void* stream);
 /* Extended term nu - N log nu per point (0 for non-extended models). */
 int ffcu_extended_terms(const ffit_model* m, const double* points, int P, double n_events,
                         double* out);
@@ -277,6 +283,54 @@ double ffcu_result_edm(const ffit_fit_result* r);
 /* fit_gradient: likelihood / gradient launches, and the per-iteration NLL trace. */
 unsigned long long ffcu_result_launches(const ffit_fit_result* r);
 int ffcu_result_trace(const ffit_fit_result* r, double* out, int cap);
+
+/* ---- event-sharded likelihood over several GPUs (csrc/shard.hpp) ----
+ * Every rank owns a contiguous range of the events of every column, resident in its HBM.
+ * A batch of P points is one fused launch per rank plus ONE collective: an NCCL all-gather
+ * of the rank's [P Neumaier pairs | P first-invalid indices] (24P bytes), then a fixed
+ * rank-order combine on the device -- the values are bitwise independent of NCCL's
+ * algorithm and identical on every rank; the extended term uses the global event count.
+ * NCCL is loaded at run time (the copy already in the process, e.g. PyTorch's, else
+ * libnccl.so.2); without it these calls fail with FFIT_ERR_NUMERIC. */
+typedef struct ffcu_shard_group ffcu_shard_group;
+#define FFCU_NCCL_ID_BYTES 128
+/* A fresh ncclUniqueId (FFCU_NCCL_ID_BYTES bytes) for create_rank: rank 0 makes it, the
+ * caller hands it to every rank (torch.distributed, MPI, a file...). */
+int ffcu_nccl_unique_id(void* id);
+/* "major.minor.patch" of the NCCL the library bound ("" when none is loadable). */
+const char* ffcu_nccl_version(void);
+/* One process per GPU: this process is global rank `rank` of `world`; `shard` (a dataset
+ * on this process's device) holds rows [offset, offset + rows) of the n_total events.  The
+ * ranks' shards must tile [0, n_total) in rank order (checked once, collectively). */
+int ffcu_shard_group_create_rank(ffit_model* m, const ffit_dataset* shard, long long n_total, long long offset,
+                                 const void* nccl_id, int world, int rank, ffcu_shard_group** out);
+/* One process, ndev distinct devices (ncclCommInitAll): host columns of n_total rows cut
+ * into ndev contiguous shards, one uploaded to each device. */
+int ffcu_shard_group_create_local(ffit_model* m, const char* const* names, const double* const* host_cols,
+                                  int ncols, long long n_total, const int* devices, int ndev,
+                                  ffcu_shard_group** out);
+void ffcu_shard_group_free(ffcu_shard_group* g);
+/* world size, local devices, n_total, and the first local device's rows / first row */
+int ffcu_shard_group_info(const ffcu_shard_group* g, int* world, int* local_devices, long long* n_total,
+                          long long* local_rows, long long* local_offset);
+/* ffcu_nll_points over all ranks' events (collective: every rank calls it with the same
+ * points; values identical on every rank). */
+int ffcu_shard_group_nll_points(ffcu_shard_group* g, const double* points, int P, double* values,
+                                long long* first_invalid, unsigned long long* n_evaluations);
+/* Asynchronous on `stream` (groups with one local device): the combined event pairs (2P
+ * doubles, no extended term) and global first-invalid indices stay on the device. */
+int ffcu_shard_group_nll_points_device(ffcu_shard_group* g, const double* points, int P, double* d_sc,
+                                       unsigned long long* d_bad, void* stream, unsigned long long* n_evaluations);
+/* ffcu_nll_grad over all ranks: per-rank slot pairs of the fused gradient pass, one
+ * all-gather, rank-order combine, host finish with the global event count. */
+int ffcu_shard_group_nll_grad(ffcu_shard_group* g, const double* points, int P, double* values, double* grads,
+                              long long* first_invalid, unsigned long long* n_evaluations);
+/* The fit drivers on the sharded likelihood (collective; the fitted values are written
+ * into the group's model on every rank): the reference's Nelder-Mead (ffit_fit) and the
+ * Minuit-style BFGS (ffcu_fit_gradient_opts; analytic as there). */
+int ffcu_shard_group_fit(ffcu_shard_group* g, double tolerance, long max_iterations, ffit_fit_result** out);
+int ffcu_shard_group_fit_gradient(ffcu_shard_group* g, double tolerance, long max_iterations, int analytic,
+                                  ffit_fit_result** out);
 
 /* Last fused-NLL launch shape: threads, events/thread, tile, tiles, chunks, grid. */
 int ffcu_last_launch(const ffit_model* m, int* info6);

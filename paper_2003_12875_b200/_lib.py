@@ -121,6 +121,20 @@ SIGNATURES = {
     "ffcu_fp64_peak": (I, [DP, ctypes.POINTER(ctypes.c_float)]),
     "ffcu_math_probe": (I, [I, DP, DP, LL]),
     "ffcu_sample_host": (I, [VP, LL, ULL, ctypes.POINTER(DP), DP]),
+    # event-sharded likelihood over several GPUs (csrc/shard.hpp)
+    "ffcu_combine_shards_device": (I, [VP, I, I, I, VP, VP, VP, VP]),
+    "ffcu_nccl_unique_id": (I, [VP]),
+    "ffcu_nccl_version": (CP, []),
+    "ffcu_shard_group_create_rank": (I, [VP, VP, LL, LL, VP, I, I, ctypes.POINTER(VP)]),
+    "ffcu_shard_group_create_local": (I, [VP, ctypes.POINTER(CP), ctypes.POINTER(DP), I, LL, IP, I,
+                                          ctypes.POINTER(VP)]),
+    "ffcu_shard_group_free": (None, [VP]),
+    "ffcu_shard_group_info": (I, [VP, IP, IP, LLP, LLP, LLP]),
+    "ffcu_shard_group_nll_points": (I, [VP, DP, I, DP, LLP, ULLP]),
+    "ffcu_shard_group_nll_points_device": (I, [VP, DP, I, VP, VP, VP, ULLP]),
+    "ffcu_shard_group_nll_grad": (I, [VP, DP, I, DP, DP, LLP, ULLP]),
+    "ffcu_shard_group_fit": (I, [VP, D, ctypes.c_long, ctypes.POINTER(VP)]),
+    "ffcu_shard_group_fit_gradient": (I, [VP, D, ctypes.c_long, I, ctypes.POINTER(VP)]),
 }
 
 

@@ -1,6 +1,7 @@
 // extern "C" boundary (include/ffit_b200.h).  Same status-code / ownership /
 // thread-local-error contract as the reference (proj/src/capi.cpp:28-50).
 #include "../../include/ffit_b200.h"
+#include "shard.hpp"
 
 #include <cmath>
 #include <cstdio>
@@ -31,6 +32,11 @@ struct ffit_dataset {
 
 struct ffit_fit_result {
   ffb::FitResult r;
+};
+
+struct ffcu_shard_group {
+  ffit_model* m = nullptr;  // the caller's model (parameters, write-back of fits)
+  std::unique_ptr<ffb::ShardGroup> g;
 };
 
 namespace {
@@ -523,6 +529,20 @@ FFB_API int ffcu_combine_pairs_device(const double* d_in, int R, int P, double* 
   });
 }
 
+FFB_API int ffcu_combine_shards_device(const double* d_in, int R, int rows, int P, const long long* d_offsets,
+                                       double* d_out, unsigned long long* d_bad, void* stream) {
+  return guarded([&] {
+    require(d_in, "d_in");
+    require(d_offsets, "d_offsets");
+    require(d_out, "d_out");
+    require(d_bad, "d_bad");
+    if (R < 1 || rows < 0 || P < 0) ffb::usage_error("combine_shards: bad sizes");
+    ffb::count_launches(ffb::launch_combine_shards(d_in, R, rows, P, d_offsets, reinterpret_cast<ffb::SumPair*>(d_out),
+                                                   d_bad, static_cast<cudaStream_t>(stream)));
+    ffb::cuda_check(cudaGetLastError(), "combine_shards");
+  });
+}
+
 FFB_API int ffcu_extended_terms(const ffit_model* m, const double* points, int P, double n_events,
                                 double* out) {
   return guarded([&] {
@@ -993,6 +1013,160 @@ FFB_API int ffcu_fit_gradient_opts(ffit_model* m, const ffit_dataset* ds, double
     if (max_iterations > 0) o.max_iterations = static_cast<int>(max_iterations);
     auto r = std::make_unique<ffit_fit_result>();
     r->r = ffb::fit_gradient(*m->m, engine(m), *ds->d, o);
+    *out = r.release();
+  });
+}
+
+// ---------------------------------------------------------------------------
+// event-sharded likelihood over several GPUs (shard.hpp)
+
+static_assert(sizeof(ncclUniqueId) == FFCU_NCCL_ID_BYTES, "NCCL unique id size");
+
+FFB_API int ffcu_nccl_unique_id(void* id) {
+  return guarded([&] {
+    require(id, "id");
+    ncclUniqueId u;
+    ffb::nccl_check(ffb::nccl().get_unique_id(&u), "ncclGetUniqueId");
+    std::memcpy(id, &u, sizeof(u));
+  });
+}
+
+FFB_API const char* ffcu_nccl_version(void) {
+  static thread_local std::string v;
+  try {
+    v = ffb::nccl().version;
+  } catch (const std::exception& e) {
+    v.clear();
+  }
+  return v.c_str();
+}
+
+FFB_API int ffcu_shard_group_create_rank(ffit_model* m, const ffit_dataset* shard, long long n_total,
+                                         long long offset, const void* nccl_id, int world, int rank,
+                                         ffcu_shard_group** out) {
+  return guarded([&] {
+    require(m, "model");
+    require(shard, "dataset");
+    require(nccl_id, "nccl_id");
+    require(out, "out");
+    ncclUniqueId u;
+    std::memcpy(&u, nccl_id, sizeof(u));
+    auto g = std::make_unique<ffcu_shard_group>();
+    g->m = m;
+    g->g = ffb::ShardGroup::create_rank(*m->m, shard->d, n_total, offset, u, world, rank);
+    *out = g.release();
+  });
+}
+
+FFB_API int ffcu_shard_group_create_local(ffit_model* m, const char* const* names, const double* const* host_cols,
+                                          int ncols, long long n_total, const int* devices, int ndev,
+                                          ffcu_shard_group** out) {
+  return guarded([&] {
+    require(m, "model");
+    require(names, "names");
+    require(host_cols, "host_cols");
+    require(devices, "devices");
+    require(out, "out");
+    if (ncols <= 0 || ndev <= 0 || n_total < 0) ffb::usage_error("shard group: bad sizes");
+    std::vector<std::string> nm;
+    std::vector<const double*> cols;
+    for (int i = 0; i < ncols; ++i) {
+      require(names[i], "column name");
+      if (n_total > 0) require(host_cols[i], "column");
+      nm.emplace_back(names[i]);
+      cols.push_back(host_cols[i]);
+    }
+    auto g = std::make_unique<ffcu_shard_group>();
+    g->m = m;
+    g->g = ffb::ShardGroup::create_local(*m->m, nm, cols, n_total, std::vector<int>(devices, devices + ndev));
+    *out = g.release();
+  });
+}
+
+FFB_API void ffcu_shard_group_free(ffcu_shard_group* g) { delete g; }
+
+FFB_API int ffcu_shard_group_info(const ffcu_shard_group* g, int* world, int* local_devices, long long* n_total,
+                                  long long* local_rows, long long* local_offset) {
+  return guarded([&] {
+    require(g, "group");
+    if (world) *world = g->g->world();
+    if (local_devices) *local_devices = g->g->local_count();
+    if (n_total) *n_total = g->g->n_total();
+    if (local_rows) *local_rows = g->g->local_rows(0);
+    if (local_offset) *local_offset = g->g->local_offset(0);
+  });
+}
+
+FFB_API int ffcu_shard_group_nll_points(ffcu_shard_group* g, const double* points, int P, double* values,
+                                        long long* first_invalid, unsigned long long* n_evaluations) {
+  return guarded([&] {
+    require(g, "group");
+    require(points, "points");
+    require(values, "values");
+    if (P < 0) ffb::usage_error("negative point count");
+    const ffb::NllResult r = g->g->nll_points(points, P);
+    std::copy(r.value.begin(), r.value.end(), values);
+    if (first_invalid) std::copy(r.first_invalid.begin(), r.first_invalid.end(), first_invalid);
+    if (n_evaluations) *n_evaluations = r.launches;
+  });
+}
+
+FFB_API int ffcu_shard_group_nll_points_device(ffcu_shard_group* g, const double* points, int P, double* d_sc,
+                                               unsigned long long* d_bad, void* stream,
+                                               unsigned long long* n_evaluations) {
+  return guarded([&] {
+    require(g, "group");
+    require(points, "points");
+    require(d_sc, "d_sc");
+    require(d_bad, "d_bad");
+    const int k = g->g->nll_points_device(points, P, reinterpret_cast<ffb::SumPair*>(d_sc), d_bad,
+                                          static_cast<cudaStream_t>(stream));
+    if (n_evaluations) *n_evaluations = static_cast<unsigned long long>(k);
+  });
+}
+
+FFB_API int ffcu_shard_group_nll_grad(ffcu_shard_group* g, const double* points, int P, double* values,
+                                      double* grads, long long* first_invalid, unsigned long long* n_evaluations) {
+  return guarded([&] {
+    require(g, "group");
+    require(points, "points");
+    require(values, "values");
+    require(grads, "grads");
+    if (P < 0) ffb::usage_error("negative point count");
+    const ffb::NllGradResult r = g->g->nll_grad_points(points, P);
+    std::copy(r.value.begin(), r.value.end(), values);
+    std::copy(r.grad.begin(), r.grad.end(), grads);
+    if (first_invalid) std::copy(r.first_invalid.begin(), r.first_invalid.end(), first_invalid);
+    if (n_evaluations) *n_evaluations = r.launches;
+  });
+}
+
+FFB_API int ffcu_shard_group_fit(ffcu_shard_group* g, double tolerance, long max_iterations, ffit_fit_result** out) {
+  return guarded([&] {
+    require(g, "group");
+    require(out, "out");
+    ffb::FitOptions o;
+    if (tolerance > 0.0) o.tolerance = tolerance;
+    if (max_iterations > 0) o.max_iterations = static_cast<int>(max_iterations);
+    auto r = std::make_unique<ffit_fit_result>();
+    r->r = ffb::fit_nelder_mead(*g->m->m, *g->g, o);
+    *out = r.release();
+  });
+}
+
+FFB_API int ffcu_shard_group_fit_gradient(ffcu_shard_group* g, double tolerance, long max_iterations, int analytic,
+                                          ffit_fit_result** out) {
+  return guarded([&] {
+    require(g, "group");
+    require(out, "out");
+    ffb::FitOptions o;
+    o.record_trace = true;
+    o.analytic_gradient = analytic < 0 ? g->g->engine(0).likelihood_plan().programs.empty() || !ffb::jit_enabled()
+                                       : analytic != 0;
+    if (tolerance > 0.0) o.tolerance = tolerance;
+    if (max_iterations > 0) o.max_iterations = static_cast<int>(max_iterations);
+    auto r = std::make_unique<ffit_fit_result>();
+    r->r = ffb::fit_gradient(*g->m->m, *g->g, o);
     *out = r.release();
   });
 }

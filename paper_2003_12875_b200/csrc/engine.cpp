@@ -18,7 +18,6 @@ namespace ffb {
 namespace {
 
 std::atomic<unsigned long long> g_launches{0};
-constexpr int kMaxPointsPerLaunch = 512;
 
 }  // namespace
 

@@ -59,6 +59,9 @@ class DeviceGuard {
   bool switched_ = false;
 };
 
+// Parameter points per device launch (larger batches are split into launches of this size).
+constexpr int kMaxPointsPerLaunch = 512;
+
 struct NllResult {
   std::vector<double> value;         // s + c + extended term; +inf if an event is invalid
   std::vector<SumPair> pairs;        // the raw per-point Neumaier pairs (events only)

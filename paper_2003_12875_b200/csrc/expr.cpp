@@ -1,3 +1,10 @@
+// The Expression formula language on the host.
+//
+// Transcribed block: the recursive-descent parser (ws / eat / next / expr / term / factor /
+// the function table and its messages) restates proj/src/expr.cpp:11-175 -- the grammar
+// and the error strings are the interface (proj/docs/expression-grammar.md; values and
+// messages are pinned bit-identical by tests/test_expr.py).  The postfix stack VM, the
+// forward-mode eval_dual and the device program lowering are new.
 #include "expr.hpp"
 
 #include <cctype>

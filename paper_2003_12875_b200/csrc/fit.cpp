@@ -1,3 +1,15 @@
+// Fit drivers over a LikelihoodSource (one device or an event-sharded group).
+//
+// Transcribed blocks (the contract of ffit_fit is "the reference's Nelder-Mead" to 1e-6,
+// which needs its iterates operation for operation; the batching into launches is new):
+//   bound_transform / _inverse     proj/src/fit.cpp:12-28
+//   invert (Gauss-Jordan)          proj/src/fit.cpp:53-84
+//   Nelder-Mead simplex + loop     proj/src/fit.cpp:108-190 (initial simplex and shrink
+//                                  issued as single multi-point launches)
+//   hessian_at (point sequence)    proj/src/fit.cpp:200-225 (all points in one launch)
+//   finish_with (write-back)       proj/src/fit.cpp:226-251
+// fit_gradient (Minuit-style BFGS on analytic or central-difference gradients) is not in
+// the reference.
 #include "fit.hpp"
 
 #include <algorithm>
@@ -31,8 +43,7 @@ constexpr double kHalfPi = 1.5707963267948966;
 // evaluates one point per nll() call).
 struct BatchObjective {
   Model& m;
-  Engine& e;
-  const DeviceDataset& ds;
+  LikelihoodSource& src;
   std::vector<int> free_ids;
   unsigned long long calls = 0, batches = 0, kernels = 0;
 
@@ -56,7 +67,7 @@ struct BatchObjective {
       const std::vector<double> th = theta_of(us[k]);
       std::copy(th.begin(), th.end(), rows.begin() + static_cast<std::ptrdiff_t>(k * npar));
     }
-    const NllResult r = e.nll_points(ds, rows.data(), static_cast<int>(us.size()));
+    const NllResult r = src.nll_points(rows.data(), static_cast<int>(us.size()));
     calls += us.size();
     batches += 1;
     kernels += r.launches;
@@ -196,15 +207,15 @@ void validate(const Model& m, const FitOptions& o, const std::vector<int>& free_
 // batched Hessian: 1 + 2d + 2d(d-1) points; analytic: 2d gradient points), before the
 // fit's clock starts: a buffer growth mid-fit re-pins host memory and frees device memory
 // (an implicit device synchronisation) at an unpredictable cost.
-static void reserve_for_fit(Model& m, Engine& e, const DeviceDataset& ds, bool analytic) {
+static void reserve_for_fit(Model& m, LikelihoodSource& src, bool analytic) {
   const int d = static_cast<int>(m.free_parameters().size());
-  e.reserve(ds, std::min(1 + 2 * d + 2 * d * std::max(d - 1, 0), 512), analytic ? 2 * d : 0);
+  src.reserve(std::min(1 + 2 * d + 2 * d * std::max(d - 1, 0), 512), analytic ? 2 * d : 0);
 }
 
-FitResult fit_nelder_mead(Model& m, Engine& e, const DeviceDataset& ds, const FitOptions& o) {
-  reserve_for_fit(m, e, ds, false);
+FitResult fit_nelder_mead(Model& m, LikelihoodSource& src, const FitOptions& o) {
+  reserve_for_fit(m, src, false);
   const auto t0 = std::chrono::steady_clock::now();
-  BatchObjective f{m, e, ds, m.free_parameters()};
+  BatchObjective f{m, src, m.free_parameters()};
   validate(m, o, f.free_ids);
   const std::size_t dim = f.free_ids.size();
   const std::vector<double> u0 = start_u(m, f.free_ids);
@@ -325,7 +336,7 @@ struct GradObjective {
         const std::vector<double> th = f.theta_of(us[k]);
         std::copy(th.begin(), th.end(), rows.begin() + static_cast<std::ptrdiff_t>(k * npar));
       }
-      const NllGradResult r = f.e.nll_grad_points(f.ds, rows.data(), static_cast<int>(us.size()));
+      const NllGradResult r = f.src.nll_grad_points(rows.data(), static_cast<int>(us.size()));
       f.calls += us.size();
       f.batches += 1;
       f.kernels += r.launches;
@@ -367,14 +378,14 @@ struct GradObjective {
 // Rounding resolution of an NLL value: a few ulps of |f|.
 static double resolution(double f) { return 4.0 * std::numeric_limits<double>::epsilon() * std::fabs(f); }
 
-FitResult fit_gradient(Model& m, Engine& e, const DeviceDataset& ds, const FitOptions& o) {
-  reserve_for_fit(m, e, ds, o.analytic_gradient && e.grad_plan().ok);
+FitResult fit_gradient(Model& m, LikelihoodSource& src, const FitOptions& o) {
+  const bool analytic = o.analytic_gradient && src.grad_ok();
+  reserve_for_fit(m, src, analytic);
   const auto t0 = std::chrono::steady_clock::now();
-  BatchObjective f{m, e, ds, m.free_parameters()};
+  BatchObjective f{m, src, m.free_parameters()};
   validate(m, o, f.free_ids);
   const std::size_t d = f.free_ids.size();
   const double h = o.fd_step;
-  const bool analytic = o.analytic_gradient && e.grad_plan().ok;
   GradObjective fg{f, analytic, h, {}};
   std::vector<double> u = start_u(m, f.free_ids);
   std::vector<double> u_prev, g_prev, u_best = u;
@@ -511,8 +522,8 @@ FitResult fit_gradient(Model& m, Engine& e, const DeviceDataset& ds, const FitOp
   return result;
 }
 
-bool hessian_uncertainties(Model& m, Engine& e, const DeviceDataset& ds, double h, FitResult& r) {
-  BatchObjective f{m, e, ds, m.free_parameters()};
+bool hessian_uncertainties(Model& m, LikelihoodSource& src, double h, FitResult& r) {
+  BatchObjective f{m, src, m.free_parameters()};
   if (f.free_ids.empty()) usage_error("no free parameters");
   finish(m, f, start_u(m, f.free_ids), h, r);
   r.n_nll_calls += f.calls;

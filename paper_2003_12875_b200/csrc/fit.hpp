@@ -49,11 +49,47 @@ struct FitResult {
 double bound_transform(double u, double lower, double upper);
 double bound_transform_inverse(double p, double lower, double upper);
 
-FitResult fit_nelder_mead(Model& m, Engine& e, const DeviceDataset& ds, const FitOptions& o);
-FitResult fit_gradient(Model& m, Engine& e, const DeviceDataset& ds, const FitOptions& o);
+// What a fit driver evaluates: the NLL (and, where the model's layout allows, its analytic
+// gradient) at a batch of parameter points, as ONE launch per batch.  EngineSource is one
+// device; ShardGroup (shard.hpp) an event-sharded likelihood over several GPUs whose batches
+// cost one collective each.
+class LikelihoodSource {
+ public:
+  virtual ~LikelihoodSource() = default;
+  virtual NllResult nll_points(const double* thetas, int P) = 0;
+  virtual NllGradResult nll_grad_points(const double* thetas, int P) = 0;
+  virtual bool grad_ok() = 0;
+  // device buffers for batches of up to P_nll likelihood / P_grad gradient points
+  virtual void reserve(int P_nll, int P_grad) = 0;
+};
+
+class EngineSource : public LikelihoodSource {
+ public:
+  EngineSource(Engine& e, const DeviceDataset& ds) : e_(e), ds_(ds) {}
+  NllResult nll_points(const double* thetas, int P) override { return e_.nll_points(ds_, thetas, P); }
+  NllGradResult nll_grad_points(const double* thetas, int P) override { return e_.nll_grad_points(ds_, thetas, P); }
+  bool grad_ok() override { return e_.grad_plan().ok; }
+  void reserve(int P_nll, int P_grad) override { e_.reserve(ds_, P_nll, P_grad); }
+
+ private:
+  Engine& e_;
+  const DeviceDataset& ds_;
+};
+
+FitResult fit_nelder_mead(Model& m, LikelihoodSource& src, const FitOptions& o);
+FitResult fit_gradient(Model& m, LikelihoodSource& src, const FitOptions& o);
+
+inline FitResult fit_nelder_mead(Model& m, Engine& e, const DeviceDataset& ds, const FitOptions& o) {
+  EngineSource src(e, ds);
+  return fit_nelder_mead(m, src, o);
+}
+inline FitResult fit_gradient(Model& m, Engine& e, const DeviceDataset& ds, const FitOptions& o) {
+  EngineSource src(e, ds);
+  return fit_gradient(m, src, o);
+}
 
 // Central-difference Hessian in u-space at the model's current values (one
 // launch of 1+2d+2d(d-1) points) -> uncertainties written into the model.
-bool hessian_uncertainties(Model& m, Engine& e, const DeviceDataset& ds, double h, FitResult& r);
+bool hessian_uncertainties(Model& m, LikelihoodSource& src, double h, FitResult& r);
 
 }  // namespace ffb

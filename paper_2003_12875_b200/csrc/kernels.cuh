@@ -73,6 +73,13 @@ int launch_eval(const DevPlan& plan, const ColPtrs& cols, long long n, const dou
 // exchange step after an all-gather): in = R x P pairs, out = P pairs.
 int launch_combine_ranks(const SumPair* d_in, int R, int P, SumPair* d_out, cudaStream_t stream);
 
+// The sharded likelihood's exchange step (shard.cpp): d_in = R rank blocks of
+// [rows pairs | P local first-invalid indices] (2 rows + P words each), gathered by one
+// collective; d_out = rows pairs combined in rank order, d_bad = P global indices
+// (d_offsets[r] = rank r's first global row).
+int launch_combine_shards(const double* d_in, int R, int rows, int P, const long long* d_offsets, SumPair* d_out,
+                          unsigned long long* d_bad, cudaStream_t stream);
+
 // Fixed-order fold of `ntiles` partial pairs per row into one pair per row.
 int launch_reduce(const SumPair* partial, int ntiles, int rows, SumPair* out, cudaStream_t stream);
 

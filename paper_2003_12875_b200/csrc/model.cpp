@@ -1,5 +1,13 @@
 // Host-side model: parser, validation, normalisation integrals.
 // See model.hpp for the reference interfaces each piece mirrors.
+//
+// Transcribed blocks (the model-file grammar and its error strings are the interface; the
+// parser is outside the hot path):
+//   to_double, tokenize, parse_call     proj/src/model.cpp:34-110
+//   Model::parse directive loop         proj/src/model.cpp:112-252 (extended with the GPU
+//                                       path's kinds: ArgusBG, Chebychev, Polynomial, ProdPdf,
+//                                       extended AddPdf, several observables -- new code)
+//   check_params messages / codes       proj/src/pdfs.cpp:127-176
 #include "model.hpp"
 
 #include <charconv>

@@ -399,6 +399,12 @@ def nll_points_device(model: Model, ds: DataSet, points, d_sc_ptr, d_bad_ptr, st
     return ne.value
 
 
+def combine_shards_device(d_in_ptr, R, rows, P, d_offsets_ptr, d_out_ptr, d_bad_ptr, stream_ptr=None):
+    """The sharded exchange's rank-order combine of R gathered [rows pairs | P indices] blocks."""
+    _check(lib().ffcu_combine_shards_device(VP(d_in_ptr), R, rows, P, VP(d_offsets_ptr), VP(d_out_ptr),
+                                            VP(d_bad_ptr), VP(stream_ptr or 0)))
+
+
 def combine_pairs_device(d_in_ptr, R, P, d_out_ptr, stream_ptr=None):
     _check(lib().ffcu_combine_pairs_device(VP(d_in_ptr), R, P, VP(d_out_ptr), VP(stream_ptr or 0)))
 
@@ -644,3 +650,123 @@ def grad_spec_source(model: Model, compile_ks=None) -> str:
 
 def last_grad_jit(model: Model) -> bool:
     return bool(lib().ffcu_last_grad_jit(model.handle))
+
+
+class ShardGroup:
+    """The event-sharded likelihood of the C ABI (ffcu_shard_group_*, csrc/shard.hpp): one
+    fused launch per rank and ONE NCCL all-gather per batch of points, combined in rank order
+    on the device.  Two ways to build one:
+
+    * ``ShardGroup.for_rank(model, shard, n_total, offset, world, rank, broadcast)`` -- one
+      process per GPU; ``broadcast(obj)`` hands rank 0's NCCL id to every rank (e.g. via
+      ``torch.distributed.broadcast_object_list``);
+    * ``ShardGroup.local(model, columns, devices)`` -- one process, several devices.
+
+    Every rank calls every method with the same points (collective); values are identical on
+    every rank.  Import torch before the first group when both share a process (one NCCL)."""
+
+    def __init__(self, handle, model, keep=None):
+        self._h = handle
+        self.model = model
+        self._keep = keep
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        _check(lib().ffcu_nccl_unique_id(buf))
+        return buf.raw
+
+    @staticmethod
+    def nccl_version() -> str:
+        return lib().ffcu_nccl_version().decode()
+
+    @classmethod
+    def for_rank(cls, model: Model, shard: DataSet, n_total: int, offset: int, world: int, rank: int,
+                 broadcast=None, nccl_id: bytes | None = None) -> "ShardGroup":
+        if nccl_id is None:
+            nid = cls.nccl_unique_id() if rank == 0 else None
+            nccl_id = broadcast(nid) if broadcast is not None else nid
+        if nccl_id is None or len(nccl_id) != 128:
+            raise FfitError(USAGE, "a 128-byte NCCL id is required on every rank")
+        buf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+        h = VP()
+        _check(lib().ffcu_shard_group_create_rank(model.handle, shard.handle, int(n_total), int(offset), buf,
+                                                  int(world), int(rank), ctypes.byref(h)))
+        return cls(h, model, keep=shard)
+
+    @classmethod
+    def local(cls, model: Model, columns: dict, devices) -> "ShardGroup":
+        names = model.observables
+        cols = [_f64(columns[n]) for n in names]
+        n = len(cols[0])
+        if any(len(c) != n for c in cols):
+            raise FfitError(USAGE, "columns have unequal lengths")
+        cn = (CP * len(names))(*[s.encode() for s in names])
+        cp = (DP * len(cols))(*[_dp(c) for c in cols])
+        devs = (ctypes.c_int * len(devices))(*[int(d) for d in devices])
+        h = VP()
+        _check(lib().ffcu_shard_group_create_local(model.handle, cn, cp, len(names), n, devs, len(devices),
+                                                   ctypes.byref(h)))
+        return cls(h, model)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and lib is not None:
+            lib().ffcu_shard_group_free(h)
+            self._h = None
+
+    def info(self) -> dict:
+        w, nl = ctypes.c_int(), ctypes.c_int()
+        nt, lr, lo = ctypes.c_longlong(), ctypes.c_longlong(), ctypes.c_longlong()
+        _check(lib().ffcu_shard_group_info(self._h, ctypes.byref(w), ctypes.byref(nl), ctypes.byref(nt),
+                                           ctypes.byref(lr), ctypes.byref(lo)))
+        return {"world": w.value, "local_devices": nl.value, "n_total": nt.value, "local_rows": lr.value,
+                "local_offset": lo.value}
+
+    def nll_points(self, points):
+        """(values[P], first_invalid[P], launches) over all ranks' events."""
+        pts = _f64(np.atleast_2d(points))
+        P = pts.shape[0]
+        vals = np.empty(P)
+        bad = np.empty(P, dtype=np.int64)
+        ne = ctypes.c_ulonglong()
+        _check(lib().ffcu_shard_group_nll_points(self._h, _dp(pts), P, _dp(vals),
+                                                 bad.ctypes.data_as(ctypes.POINTER(ctypes.c_longlong)),
+                                                 ctypes.byref(ne)))
+        return vals, bad, ne.value
+
+    def nll_points_device(self, points, d_sc_ptr, d_bad_ptr, stream_ptr=None) -> int:
+        """Async on a CUDA stream: combined pairs (2P doubles, no extended term) and global
+        first-invalid indices (P uint64) into device buffers."""
+        pts = _f64(np.atleast_2d(points))
+        ne = ctypes.c_ulonglong()
+        _check(lib().ffcu_shard_group_nll_points_device(self._h, _dp(pts), pts.shape[0], VP(d_sc_ptr),
+                                                        VP(d_bad_ptr), VP(stream_ptr or 0), ctypes.byref(ne)))
+        return ne.value
+
+    def nll_grad(self, points):
+        """(values[P], grads[P, npar], first_invalid[P], launches) over all ranks' events."""
+        pts = _f64(np.atleast_2d(points))
+        P = pts.shape[0]
+        npar = len(self.model.param_names)
+        vals = np.empty(P)
+        grads = np.empty((P, npar))
+        bad = np.empty(P, dtype=np.int64)
+        ne = ctypes.c_ulonglong()
+        _check(lib().ffcu_shard_group_nll_grad(self._h, _dp(pts), P, _dp(vals), _dp(grads),
+                                               bad.ctypes.data_as(ctypes.POINTER(ctypes.c_longlong)),
+                                               ctypes.byref(ne)))
+        return vals, grads, bad, ne.value
+
+    def fit(self, tolerance=0.0, max_iterations=0) -> "FitResult":
+        """The reference's Nelder-Mead on the sharded likelihood (fitted values -> model)."""
+        h = VP()
+        _check(lib().ffcu_shard_group_fit(self._h, tolerance, max_iterations, ctypes.byref(h)))
+        return _result(h)
+
+    def fit_gradient(self, tolerance=0.0, max_iterations=0, analytic=None) -> "FitResult":
+        """Minuit-style BFGS on the sharded likelihood (as fit_gradient)."""
+        h = VP()
+        flag = -1 if analytic is None else (1 if analytic else 0)
+        _check(lib().ffcu_shard_group_fit_gradient(self._h, tolerance, max_iterations, flag, ctypes.byref(h)))
+        return _result(h)

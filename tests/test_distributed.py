@@ -42,66 +42,118 @@ def test_combine_is_fixed_order_and_compensated():
     assert np.array_equal(D.combine_pairs(pairs), out)
 
 
-def _worker(rank, world, port, q):
+def _spawn(target, world=2, timeout=300, args=()):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=target, args=(r, world, port, q) + args) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = q.get(timeout=timeout)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return out
+
+
+def _init(rank, world, port):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    import torch
+    return dist
 
+
+def _oracle_partial(o, shard, n_local):
+    """CPU stand-in for the GPU's per-rank launch: the oracle's Neumaier sum over this
+    rank's events (no extended term) and its local first invalid event."""
+    def partial(pts):
+        pairs = np.zeros((len(pts), 2))
+        bad = np.full(len(pts), -1, dtype=np.int64)
+        for p, th in enumerate(pts):
+            _, comp, bi = o.nll(shard, th)
+            if bi >= 0:
+                bad[p] = bi
+            else:
+                pairs[p] = (comp - o.extended_term(n_local, th), 0.0)
+        return pairs, bad
+    return partial
+
+
+def _worker(rank, world, port, q, case):
+    dist = _init(rank, world, port)
+    import paper_2003_12875_b200 as fb
     from oracle.oracle import OracleModel
     from paper_2003_12875_b200 import configs
 
     w = configs.C4  # extended model: the extended term needs the global N
+    m = fb.Model.from_string(w.text)
     o = OracleModel(w.text)
     n = 30_001
     cols, _ = o.sample(n, 7)
-    pts = w.points(type("M", (), {"param_names": o.param_names, "theta": lambda self=None: o.theta.copy()}),
-                   n_points=4)
+    if case == "invalid":
+        cols[0][20_000] = np.nan  # non-finite data: invalid event (proj/src/eval.cpp:138-145)
+        cols[0][25_000] = np.inf
+    P = 600 if case == "many" else 4
+    pts = w.points(m, n_points=P)
     b, e = D.shard_bounds(n, world, rank)
     shard = [c[b:e] for c in cols]
-    # local partial pairs: the oracle's Neumaier sum of this shard's events (no extended term)
-    local = np.zeros((4, 2))
-    bad = np.full(4, -1, dtype=np.int64)
-    for p in range(4):
-        _, comp, bi = o.nll(shard, pts[p])
-        local[p] = (comp - o.extended_term(e - b, pts[p]), 0.0)
-        bad[p] = bi
-    t = torch.from_numpy(local)
-    gathered = [torch.zeros_like(t) for _ in range(world)]
-    dist.all_gather(gathered, t)
-    tb = torch.from_numpy(bad)
-    gb = [torch.zeros_like(tb) for _ in range(world)]
-    dist.all_gather(gb, tb)
-    offs = [D.shard_bounds(n, world, r)[0] for r in range(world)]
-    combined = D.combine_pairs(np.stack([g.numpy() for g in gathered]))
-    gbad = D.first_invalid_global(np.stack([g.numpy() for g in gb]), offs)
-    ext = np.array([o.extended_term(n, pts[p]) for p in range(4)])
-    vals = D.finalize(combined, gbad, ext)
+    snll = D.ShardedNll(m, None, n, b, dist, n_local=e - b, partial=_oracle_partial(o, shard, e - b))
+    vals = snll.nll_points(pts)
+    bad = snll.first_invalid.copy()
     if rank == 0:
-        full = np.array([o.nll(cols, pts[p])[1] for p in range(4)])
-        q.put((vals, full))
+        check = [0, P - 1] if P > 4 else list(range(P))
+        full = [o.nll(cols, pts[p]) for p in check]
+        q.put((vals[check], bad[check], np.array([f[1] for f in full]), np.array([f[2] for f in full]),
+               snll.offsets))
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_two_rank_gloo_sharded_nll_matches_single_process():
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
-    for p in procs:
-        p.start()
-    vals, full = q.get(timeout=240)
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
-    assert np.all(np.abs(vals - full) <= 1e-12 * np.abs(full))
+@pytest.mark.parametrize("case", ["plain", "invalid", "many"])
+def test_two_rank_gloo_sharded_nll_drives_the_product_class(case):
+    """ShardedNll itself at world_size 2 over gloo: one all-gather of the packed
+    [pairs | first-invalid] block per launch (600 points: two launches), rank-order combine,
+    global first-invalid index, extended term with the global N -- equal to one process."""
+    vals, bad, full, fbad, offsets = _spawn(_worker, args=(case,))
+    assert offsets == [0, 15_000]
+    assert np.array_equal(bad, fbad)
+    if case == "invalid":
+        assert np.all(bad == 20_000) and np.all(np.isinf(vals))
+    else:
+        assert np.all(bad == -1)
+        assert np.all(np.abs(vals - full) <= 1e-12 * np.abs(full))
+
+
+def _tiling_worker(rank, world, port, q):
+    dist = _init(rank, world, port)
+    import paper_2003_12875_b200 as fb
+    from paper_2003_12875_b200 import configs
+    m = fb.Model.from_string(configs.C1.text)
+    try:
+        D.ShardedNll(m, None, 100, 10 * rank, dist, n_local=10)  # rank 1 starts at 10, ends at 20: rows missing
+        err = None
+    except ValueError as e:
+        err = str(e)
+    if rank == 0:
+        q.put(err)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_nll_checks_the_tiling_once():
+    err = _spawn(_tiling_worker)
+    assert err is not None and "n_total is 100" in err
 
 
 def test_first_invalid_global_index():
     bad = np.array([[-1, 5], [3, -1]])
     assert list(D.first_invalid_global(bad, [0, 100])) == [103, 5]
+    # the packed exchange block round trip (the C ABI's layout: pairs, then int64 indices)
+    blocks = np.stack([D.pack(np.array([[1.0, 1e-17], [2.0, 0.0]]), np.array([-1, 5])),
+                       D.pack(np.array([[3.0, 0.0], [4.0, 2e-17]]), np.array([3, -1]))])
+    pairs, gbad = D.combine_packed(blocks, 2, 2, [0, 100])
+    assert list(gbad) == [103, 5] and pairs[0, 0] == 4.0 and pairs[1, 1] == 2e-17
     vals = D.finalize(np.zeros((2, 2)), np.array([-1, 7]), np.zeros(2))
     assert vals[0] == 0 and np.isinf(vals[1])
 
@@ -131,12 +183,7 @@ def _c2_slots(o, names, coefs, cols_x, theta):
 
 
 def _grad_worker(rank, world, port, q):
-    import torch.distributed as dist
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    import torch
-
+    dist = _init(rank, world, port)
     import paper_2003_12875_b200 as fb
     from oracle.oracle import OracleModel
     from paper_2003_12875_b200 import configs
@@ -151,12 +198,12 @@ def _grad_worker(rank, world, port, q):
     coefs = m.point_constants(th)[[t["coff"] for t in terms]]
     assert fb.grad_slot_count(m) == 6
     b, e = D.shard_bounds(n, world, rank)
-    local = _c2_slots(o, m.param_names, coefs, cols[0][b:e], th)[None]  # [P=1, S, 2]
-    t = torch.from_numpy(local)
-    gathered = [torch.zeros_like(t) for _ in range(world)]
-    dist.all_gather(gathered, t)
-    sums = D.combine_slots(np.stack([g.numpy() for g in gathered]))
-    vals, grads = fb.nll_grad_finish(m, th[None], sums, n)
+
+    def grad_partial(pts):  # CPU stand-in for the fused gradient pass on this shard
+        return _c2_slots(o, m.param_names, coefs, cols[0][b:e], pts[0])[None], np.full(1, -1, dtype=np.int64)
+
+    snll = D.ShardedNll(m, None, n, b, dist, n_local=e - b, grad_partial=grad_partial)
+    vals, grads = snll.nll_grad(th[None])
     if rank == 0:
         q.put((vals, grads, th, cols[0]))
     dist.barrier()
@@ -170,16 +217,7 @@ def test_two_rank_gloo_sharded_gradient():
 
     from oracle.oracle import OracleModel
     from paper_2003_12875_b200 import configs
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_grad_worker, args=(r, 2, port, q)) for r in range(2)]
-    for p in procs:
-        p.start()
-    vals, grads, th, x = q.get(timeout=240)
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
+    vals, grads, th, x = _spawn(_grad_worker)
     o = OracleModel(configs.C2.text)
     _, comp, _ = o.nll([x], th)
     assert abs(vals[0] - comp) <= 1e-12 * abs(comp)
