@@ -43,17 +43,87 @@ def lib():
     return _lib
 
 
-def ref_available():
-    return os.path.exists(REF_SO)
+def ref_available(variant=None):
+    return os.path.exists(ref_path(variant))
 
 
-def ref():
+def ref_path(variant=None):
+    """oracle/_ref builds: None = the reference's Release flags (baseline x86-64), "v3" /
+    "v4" = the same sources with -march=x86-64-v3 / -v4 (oracle/Makefile)."""
+    return REF_SO if not variant else os.path.join(HERE, "_ref", f"libffit_ref_{variant}.so")
+
+
+_ref_variants = {}
+
+
+def ref(variant=None):
     global _ref
-    if _ref is None:
-        L = ctypes.CDLL(REF_SO)
+    if not variant:
+        if _ref is None:
+            L = ctypes.CDLL(REF_SO)
+            L.ref_last_error.restype = ctypes.c_char_p
+            _ref = L
+        return _ref
+    if variant not in _ref_variants:
+        L = ctypes.CDLL(ref_path(variant))
         L.ref_last_error.restype = ctypes.c_char_p
-        _ref = L
-    return _ref
+        _ref_variants[variant] = L
+    return _ref_variants[variant]
+
+
+def host_isa_levels():
+    """The oracle/_ref ISA builds this host CPU can run (from /proc/cpuinfo flags)."""
+    try:
+        flags = set()
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("flags"):
+                    flags = set(line.split(":", 1)[1].split())
+                    break
+    except OSError:
+        return []
+    out = []
+    if {"avx2", "fma", "bmi2", "movbe"} <= flags:
+        out.append("v3")
+        if {"avx512f", "avx512bw", "avx512cd", "avx512dq", "avx512vl"} <= flags:
+            out.append("v4")
+    return out
+
+
+class RefColumn:
+    """A reference DataSet (one column) inside one ISA build of oracle/_ref."""
+
+    def __init__(self, variant, name, col):
+        self.variant = variant
+        self.L = ref(variant)
+        self.col = np.ascontiguousarray(col, dtype=np.float64)
+        self.h = ctypes.c_void_p()
+        rc = self.L.ref_dataset_create(name.encode(), _dp(self.col), _LL(len(self.col)), ctypes.byref(self.h))
+        if rc:
+            raise OracleError(rc, self.L.ref_last_error().decode())
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.L.ref_dataset_free(self.h)
+            self.h = None
+
+    def nll_points(self, text, names, points, threads, mode=1):
+        """ref_nll_points_threaded: P points over `threads` host threads, each with its own
+        reference Model over this DataSet."""
+        points = np.ascontiguousarray(points, dtype=np.float64)
+        P = points.shape[0]
+        out = np.empty(P)
+        arr = (ctypes.c_char_p * len(names))(*[n.encode() for n in names])
+        rc = self.L.ref_nll_points_threaded(text.encode(), self.h, mode, arr, len(names), _dp(points), P, threads,
+                                            _dp(out))
+        if rc:
+            raise OracleError(rc, self.L.ref_last_error().decode())
+        return out
+
+
+def ref_nll_points_variant(variant, text, column, col, names, points, threads, mode=1):
+    """ref_nll_points_threaded on one ISA build (a DataSet made for the call)."""
+    return RefColumn(variant, column, col).nll_points(text, names, points, threads, mode)
 
 
 def _dp(a):

@@ -110,6 +110,13 @@ DriverApi& driver() {
 
 std::atomic<bool> g_enabled{std::getenv("FFB_NO_EXPR_JIT") == nullptr};
 std::mutex g_mu;
+
+// FFB_JIT_OPTS (extra NVRTC options, read at every compile) is part of every build cache key:
+// a process can hold a build and its A/B variant side by side (bench.py's per-event-log line).
+std::string opts_key() {
+  const char* e = std::getenv("FFB_JIT_OPTS");
+  return e ? std::string("\n// opts: ") + e : std::string();
+}
 std::string g_status = "not used yet";
 
 constexpr int kJitThreads = 256;
@@ -755,7 +762,7 @@ SpecModule* spec_module(const HostPlan& plan, const GradPlan& gp, int ks) {
   int dev = 0;
   cudaGetDevice(&dev);
   const std::string src = grad_spec_source(plan, gp);
-  const auto key = std::make_tuple(dev, src, ks);
+  const auto key = std::make_tuple(dev, src + opts_key(), ks);
   std::lock_guard<std::mutex> lk(g_mu);
   auto it = g_spec.find(key);
   if (it != g_spec.end()) return it->second.mod ? &it->second : nullptr;
@@ -879,7 +886,7 @@ Module* module_for(const HostPlan& plan, const ExprHoist* hoist) {
   int dev = 0;
   cudaGetDevice(&dev);
   const std::string src = full_source(plan, hoist);
-  const auto key = std::make_pair(dev, src);
+  const auto key = std::make_pair(dev, src + opts_key());
   std::lock_guard<std::mutex> lk(g_mu);
   auto it = g_modules.find(key);
   if (it != g_modules.end()) return it->second.mod ? &it->second : nullptr;
@@ -1058,7 +1065,7 @@ PlanModule* plan_module(const DevPlan& d, int ks) {
   int dev = 0;
   cudaGetDevice(&dev);
   const std::string src = plan_spec_source(d);
-  const auto key = std::make_tuple(dev, src, spec_mode(d, ks));
+  const auto key = std::make_tuple(dev, src + opts_key(), spec_mode(d, ks));
   std::lock_guard<std::mutex> lk(g_mu);
   auto it = g_plan_mods.find(key);
   if (it != g_plan_mods.end()) return it->second.mod ? &it->second : nullptr;

@@ -420,6 +420,13 @@ def probabilities(model: Model, ds: DataSet, mode: EvalMode = EvalMode.Gpu, poin
     return out
 
 
+def eval_batch_device(model: Model, pdf: str | None, ds: DataSet, d_out_ptr, stream_ptr=None):
+    """Unnormalised values of a named pdf into a device buffer (n doubles), asynchronous on
+    a CUDA stream (None: the model's own stream)."""
+    _check(lib().ffcu_eval_batch_device(model.handle, pdf.encode() if pdf else None, ds.handle, VP(d_out_ptr),
+                                        VP(stream_ptr or 0)))
+
+
 def eval_batch(model: Model, pdf: str, ds: DataSet) -> np.ndarray:
     """PdfSpec::eval_batch (proj/src/pdfs.cpp:212-269): unnormalised values of a named pdf."""
     out = np.empty(ds.n_rows)

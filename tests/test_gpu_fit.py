@@ -61,22 +61,29 @@ def test_gradient_fit_reaches_reference_minimum(name, analytic):
     r = fb.fit_gradient(m, ds, tolerance=1e-12, max_iterations=200, analytic=analytic)
     assert r.converged
     assert r.analytic_gradient == analytic
+    # the achievable agreement: the reference's Nelder-Mead stops once its simplex's NLL
+    # spread is below tol, i.e. anywhere with NLL - NLL_min <~ tol, up to sqrt(2 tol) sigma
+    # from the minimum in any direction (x10 for a minimum outside the final simplex); the
+    # gradient fit ends with a Newton step on the full Hessian, ~1e-6 sigma from it
     for p in r.parameters:
         want, unc = gold["params"][p.name]
-        assert abs(p.value - want) <= max(1e-6, 2e-3 * unc), (p.name, p.value, want)
+        bound = 10.0 * np.sqrt(2.0 * case["tol"]) * unc + 1e-9 * max(1.0, abs(want))
+        assert abs(p.value - want) <= bound, (p.name, p.value, want, bound)
     assert r.nll_min <= gold["nll"] + 1e-7
     assert r.uncertainties_valid
     for p in r.parameters:  # the reference's Hessian uncertainties
         assert p.uncertainty == pytest.approx(gold["params"][p.name][1], rel=1e-3)
     d = len(r.parameters)
     hess = 1 + 2 * d + 2 * d * (d - 1)  # the one Hessian launch
+    L = r.n_launches
     if analytic:
-        # the start launch (centre + 2d gradient points), one point per launch, then the
-        # Hessian from the gradients at u +- h e_i (2d points, one launch)
-        assert r.n_nll_calls == (2 * d + 1) + (r.n_launches - 2) + 2 * d
+        # the start launch (centre + 2d gradient points), one point per launch, the Hessian
+        # from the gradients at u and u +- h e_i (2d+1 points, one launch), and the Newton
+        # step (one point) if it was predicted to gain
+        assert r.n_nll_calls in ((2 * d + 1) + (L - 3) + (2 * d + 1) + 1, (2 * d + 1) + (L - 2) + (2 * d + 1))
     else:
-        # every iteration is one launch of 2d+1 points
-        assert r.n_nll_calls == (r.n_launches - 1) * (2 * d + 1) + hess
+        # every iteration is one launch of 2d+1 points, the Hessian one launch, the Newton step
+        assert r.n_nll_calls in ((L - 2) * (2 * d + 1) + hess + 1, (L - 1) * (2 * d + 1) + hess)
 
 
 def test_fit_nll_matches_oracle_at_minimum():
@@ -99,3 +106,41 @@ def test_hessian_points_batched_into_one_launch():
     for p in r.parameters:
         assert abs(p.value - gold["params"][p.name][0]) <= 5 * p.uncertainty * 1e-3 + 1e-6
     assert np.isfinite(r.nll_min)
+
+
+C5_GOLD = os.path.join(os.path.dirname(__file__), "golden", "c5_cpu_fit.json")
+
+
+@pytest.mark.slow
+def test_c5_fit_matches_the_cpu_fit():
+    """BASELINE config 5: the config-2 model at 2e8 events with 5 free parameters (m0 free),
+    fitted on the GPU -- BFGS on central differences (2d+1 points per launch), on the fused
+    analytic gradient, and through the event-sharded group (ffcu_shard_group_fit_gradient,
+    one rank here) -- against the CPU fit (tests/golden/make_c5_fit.py: Newton on the
+    oracle's NLL over all 2e8 events, converged to 1e-6 sigma): every fitted parameter
+    within 1e-6 (absolute), the minimum NLL within 1e-12, the uncertainties within 1 %."""
+    from paper_2003_12875_b200 import configs
+    gold = json.load(open(C5_GOLD))
+    w = configs.C5
+    assert gold["workload"] == w.name and gold["n_events"] == w.n_events
+    truth = fb.Model.from_string(w.text)
+    cols, _ = fb.sample_host(truth, w.n_events, w.data_seed)
+    ds = fb.DataSet.from_columns(cols)
+    del cols
+    for how in ("fd", "analytic", "sharded"):
+        m = fb.Model.from_string(w.text)
+        for k, v in gold["start"].items():
+            m.set(k, v)
+        if how == "sharded":
+            pytest.importorskip("torch")
+            r = fb.ShardGroup.for_rank(m, ds, w.n_events, 0, 1, 0).fit_gradient(tolerance=1e-12, max_iterations=100,
+                                                                               analytic=False)
+        else:
+            r = fb.fit_gradient(m, ds, tolerance=1e-12, max_iterations=100, analytic=how == "analytic")
+        assert r.converged, how
+        assert set(p.name for p in r.parameters) == set(gold["parameters"])
+        for p in r.parameters:
+            want = gold["parameters"][p.name]
+            assert abs(p.value - want) <= 1e-6, (how, p.name, p.value, want, p.value - want)
+            assert p.uncertainty == pytest.approx(gold["sigma"][p.name], rel=1e-2), (how, p.name)
+        assert abs(r.nll_min - gold["nll_min"]) <= 1e-12 * abs(gold["nll_min"]), (how, r.nll_min, gold["nll_min"])

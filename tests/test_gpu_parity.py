@@ -989,3 +989,71 @@ def test_more_points_than_one_launch():
     # the second chunk alone (512 points: the same kernel shape as inside the big call)
     v2, _, _ = fb.nll_points(m, ds, pts[512:1024])
     assert np.array_equal(np.asarray(v2), np.asarray(vals[512:1024]))
+
+
+def test_upload_stream_pipeline_is_bit_identical():
+    """The double-buffered pipeline bench.py's e2e runs (ffcu_dataset_copy_from_host_async into
+    the other of two datasets on a copy stream; ffcu_nll_points_device_upload copying the
+    constant rows on that stream; the next step queued before the current one's results are
+    read), with DIFFERENT events and points every step, interleaved with eval_batch_device on
+    the model's own stream: every step's pairs equal ffcu_nll_points_partial on the same
+    events and points, bit for bit (an ordering bug would mix rows or events of two steps)."""
+    torch = pytest.importorskip("torch")
+    w = configs.C2
+    m = fb.Model.from_string(w.text)
+    n, P, steps = 300_007, 12, 8
+    data = [fb.sample_host(m, n, 5000 + i)[0]["x"] for i in range(steps)]
+    pts = [w.points(m, n_points=P, seed=7000 + i) for i in range(steps)]
+    dev = torch.device("cuda", 0)
+    pinned = [torch.from_numpy(x).pin_memory() for x in data]
+    bufs = [fb.DataSet.from_columns({"x": data[0]}), fb.DataSet.from_columns({"x": data[1]})]
+    stream, copy_stream = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+    copied = [torch.cuda.Event() for _ in bufs]
+    done = [torch.cuda.Event() for _ in bufs]
+    d_sc = [torch.empty((P, 2), dtype=torch.float64, device=dev) for _ in range(steps)]
+    d_bad = [torch.empty(P, dtype=torch.int64, device=dev) for _ in range(steps)]
+    d_eval = torch.empty(n, dtype=torch.float64, device=dev)
+    for i in range(steps):
+        k = i % 2
+        copy_stream.wait_event(done[k])
+        bufs[k].copy_from_host_async({"x": pinned[i].numpy()}, copy_stream.cuda_stream)
+        copied[k].record(copy_stream)
+        stream.wait_event(copied[k])
+        fb.nll_points_device(m, bufs[k], pts[i], d_sc[i].data_ptr(), d_bad[i].data_ptr(), stream.cuda_stream,
+                             copy_stream.cuda_stream)
+        if i % 3 == 1:  # a per-event evaluation on the model's own stream between steps
+            fb.eval_batch_device(m, "sig", bufs[k], d_eval.data_ptr(), None)
+        done[k].record(stream)
+    torch.cuda.synchronize()
+    for i in range(steps):
+        want, wbad = fb.nll_points_partial(m, fb.DataSet.from_columns({"x": data[i]}), pts[i])
+        got = d_sc[i].cpu().numpy()
+        assert np.array_equal(got, want), i
+        assert np.all(d_bad[i].cpu().numpy() == -1) and np.all(wbad == -1)
+
+
+@pytest.mark.slow
+def test_c4_full_size_parity_and_properties():
+    """configs[3] at its full size, the bench's headline launch (1e8 events x 64 points,
+    extended): oracle parity at four points (threaded oracle), shard additivity over four
+    contiguous shards combined in rank order with the extended term on the global N, and
+    permutation invariance."""
+    w = configs.C4
+    m, ds, cols, o = setup(w.text, w.n_events, w.data_seed)
+    n = w.n_events
+    pts = w.points(m)
+    assert len(pts) == 64
+    vals, bad, _ = fb.nll_points(m, ds, pts)
+    assert np.all(bad == -1) and np.all(np.isfinite(vals))
+    sel = [0, 21, 42, 63]
+    comp = o.nll_points(cols, pts[sel], threads=4)
+    assert np.all(np.abs(vals[sel] - comp) <= NLL_TOL * np.abs(comp)), (vals[sel] - comp) / comp
+    parts = np.stack([fb.nll_points_partial(m, ds.slice(b, e), pts)[0]
+                      for b, e in (D.shard_bounds(n, 4, r) for r in range(4))])
+    comb = D.combine_pairs(parts).sum(axis=1) + m.extended_terms(pts, n)
+    assert np.all(np.abs(comb - vals) <= NLL_TOL * np.abs(vals))
+    perm = np.random.default_rng(0).permutation(n)
+    shuffled = fb.DataSet.from_columns({"x": cols[0][perm]})
+    del perm
+    sv, _, _ = fb.nll_points(m, shuffled, pts[:8])
+    assert np.all(np.abs(sv - vals[:8]) <= NLL_TOL * np.abs(vals[:8]))

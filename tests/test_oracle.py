@@ -282,3 +282,56 @@ def test_oracle_exp_edges_bit_exact(name):
     assert o.normalization() == sc[3]
     if name != "expo_overflow_edge":
         assert 0.0 < p[p > 0].min() < 2.2250738585072014e-308  # the case exercises the window
+
+
+# ---------------------------------------------------------------- the reference arm's spelling
+
+def _ref_arm_nll(w, cols_by_name, pts, variant=None, mode=1):
+    from oracle.oracle import ref_nll_points_variant
+    from paper_2003_12875_b200 import configs
+    arm = configs.REF_ARMS[w.name]
+    total = np.zeros(len(pts))
+    for part in arm.parts:
+        total += ref_nll_points_variant(variant, part.text, part.column, cols_by_name[part.column], part.names,
+                                        part.rows(pts), 2, mode)
+    if arm.extended is not None:
+        total += arm.extended(pts, len(next(iter(cols_by_name.values()))))
+    return total
+
+
+@pytest.mark.skipif(not __import__("oracle.oracle", fromlist=["x"]).ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("idx", range(5))
+def test_reference_arm_spelling_matches_the_oracle(idx):
+    """bench.py --impl reference runs each BASELINE workload through the unmodified reference
+    engine as configs.REF_ARMS spells it (C3: three 1-D NLLs; C4: WeightedSum with fractions
+    y/nu plus nu - N log nu; ArgusBG / Chebychev as Expression pdfs).  That decomposition
+    equals the workload's NLL (the oracle, = the product's semantics) to 1e-12 -- which also
+    pins the ProdPdf and extended-term semantics against the reference itself."""
+    from paper_2003_12875_b200 import configs
+    w = configs.BY_INDEX[idx]
+    o = OracleModel(w.text)
+    cols, _ = o.sample(20_011, w.data_seed)
+    by = {name: c for (name, _, _), c in zip(o.obs, cols)}
+    pts = w.points(type("M", (), {"param_names": o.param_names, "theta": lambda self=None: o.theta.copy()}),
+                   n_points=3)
+    want = np.array([o.nll(cols, p)[1] for p in pts])
+    got = _ref_arm_nll(w, by, pts)
+    assert np.all(np.abs(got - want) <= 1e-12 * np.abs(want)), (got - want) / want
+
+
+@pytest.mark.skipif(not all(__import__("oracle.oracle", fromlist=["x"]).ref_available(v) for v in ("v3", "v4")),
+                    reason="ISA builds of oracle/_ref not built")
+def test_isa_builds_of_the_reference_give_the_same_bits():
+    """The -march=x86-64-v3 / -v4 builds (the "-march=native" CPU-baseline variants) compute the
+    same values as the Release build (-std=c++20: no FMA contraction), in both batch modes."""
+    from oracle.oracle import host_isa_levels
+    from paper_2003_12875_b200 import configs
+    w = configs.C4
+    o = OracleModel(w.text)
+    cols, _ = o.sample(5_003, w.data_seed)
+    pts = w.points(type("M", (), {"param_names": o.param_names, "theta": lambda self=None: o.theta.copy()}),
+                   n_points=2)
+    for mode in (1, 2):
+        base = _ref_arm_nll(w, {"x": cols[0]}, pts, None, mode)
+        for v in host_isa_levels():
+            assert np.array_equal(_ref_arm_nll(w, {"x": cols[0]}, pts, v, mode), base), (v, mode)
