@@ -1110,6 +1110,7 @@ std::string plan_spec_struct(const DevPlan& d) {
        "  static constexpr bool kOn = true;\n"
     << "  static constexpr int nterms = " << d.nterms << ";\n"
     << "  static constexpr bool simple = " << (d.simple ? "true" : "false") << ";\n"
+    << "  static constexpr int stride = " << d.stride << ";\n"
     << "  static constexpr DevTerm t[" << d.nterms << "] = {";
   for (int i = 0; i < d.nterms; ++i) {
     const DevTerm& t = d.t[i];
@@ -1134,7 +1135,7 @@ std::string plan_spec_source(const DevPlan& d) {
   // instead of 64-bit immediates materialised per use (A/B, profiles/r01_ab1: +0.2-2.3 %
   // on C2-C4, -0.5 % on C1)
   return "// generated by jit.cpp: the launch's term list for nll_kernel<..., PlanSpec>\n"
-         "#define FFB_CONST_BANK 1\n" +
+         "#define FFB_CONST_BANK 1\n#define FFB_NLL_ITEM_LOOP 1\n" +
          plan_spec_struct(d) + "#include \"kernels_device.cuh\"\n";
 }
 
@@ -1226,8 +1227,9 @@ NllLaunchInfo launch_nll_spec(const DevPlan& launch, const ColPtrs& cols, long l
   const int nchunks = (P + pchunk - 1) / pchunk;
   void* args[] = {&dp, &cp, &nn, &kc, &PP, &pchunk, &ntiles, &partial, &bad};
   if (ev_start) cudaEventRecord(ev_start, stream);
+  const long long grid = nll_grid(static_cast<long long>(ntiles) * nchunks, slots);
   const CUresult rc =
-      drv.launch(m->fn, static_cast<unsigned>(static_cast<long long>(ntiles) * nchunks), 1, 1, kJitThreads, 1, 1,
+      drv.launch(m->fn, static_cast<unsigned>(grid), 1, 1, kJitThreads, 1, 1,
                  (launch.ncols + launch.ncached) * stile * sizeof(double),
                  reinterpret_cast<CUstream>(stream), args, nullptr);
   if (ev_stop) cudaEventRecord(ev_stop, stream);
@@ -1238,7 +1240,7 @@ NllLaunchInfo launch_nll_spec(const DevPlan& launch, const ColPtrs& cols, long l
   info.tile = stile;
   info.ntiles = ntiles;
   info.nchunks = nchunks;
-  info.grid = ntiles * nchunks;
+  info.grid = static_cast<int>(grid);
   info.launches = 2;
   info.jit = 2;
   return info;

@@ -86,6 +86,9 @@ int launch_reduce(const SumPair* partial, int ntiles, int rows, SumPair* out, cu
 // Target waves of the tile kernel's (tile x point-chunk) grid (FFB_NLL_WAVES).
 int nll_waves();
 
+// The tile kernel's grid for `items` work items on `slots` resident CTAs (FFB_NLL_PERSIST).
+long long nll_grid(long long items, long long slots);
+
 // Streaming multiprocessors of the current device (cached).
 int device_sm_count();
 
