@@ -6,7 +6,7 @@ package is its Python mirror of the reference interface.
 """
 from ._lib import LIB_PATH, build, lib  # noqa: F401
 from .ffit import (  # noqa: F401
-    DataSet, EvalMode, FfitError, FitResult, Model, NllValue, ShardGroup, eval_batch, expr_eval, expression_jit,
+    DataSet, EvalMode, FfitError, FitResult, Model, NllValue, ShardGroup, eval_batch, eval_batch_device, expr_eval, expression_jit,
     expression_jit_source, expression_jit_status, fit_gradient, fit_to, grad_spec_source, last_grad_jit,
     last_launch_jit, last_launch_cached, plan_spec_min_work, plan_spec_source,
     fp64_peak, kernel_launches, kernel_timer, kernel_timer_read, last_launch, nll, nll_c, nll_points,

@@ -168,12 +168,15 @@ bool hessian_at(BatchObjective& f, const std::vector<double>& u_min, double h,
   return invert(hess);
 }
 
+// Rounding resolution of an NLL value: a few ulps of |f|.
+double resolution(double f) { return 4.0 * std::numeric_limits<double>::epsilon() * std::fabs(f); }
+
 // One Newton step from a BFGS minimum on the inverted u-space Hessian of the uncertainty
 // estimate and the gradient at the same point (not in the reference; fit_gradient only).
 // BFGS stops once its estimated distance to the minimum (EDM) is below the NLL's own
 // rounding -- on a 2e8-event NLL ~ 5e8 that leaves it up to ~1e-3 sigma from the minimum;
 // the full Hessian's step lands within the gradient's noise, for one more NLL point.  The
-// step is kept only if the NLL does not rise.
+// step is kept unless the NLL rises beyond its rounding.
 void newton_polish(BatchObjective& f, std::vector<double>& u, double& f_u, const std::vector<double>& g,
                    const std::vector<std::vector<double>>& hinv, FitResult& r) {
   const std::size_t d = u.size();
@@ -187,7 +190,9 @@ void newton_polish(BatchObjective& f, std::vector<double>& u, double& f_u, const
   }
   if (!(pred > 0.0) || !std::isfinite(pred)) return;
   const double fn = f.one(un);
-  if (std::isfinite(fn) && fn <= f_u) {
+  // kept unless the NLL rises by more than its own rounding: a step whose predicted gain is
+  // below the rounding cannot be judged by the NLL value, only by the model
+  if (std::isfinite(fn) && fn <= f_u + resolution(f_u)) {
     u = un;
     f_u = fn;
     r.edm = 0.0;  // the step was the model's own estimate of the remaining distance
@@ -405,8 +410,6 @@ struct GradObjective {
 
 }  // namespace
 
-// Rounding resolution of an NLL value: a few ulps of |f|.
-static double resolution(double f) { return 4.0 * std::numeric_limits<double>::epsilon() * std::fabs(f); }
 
 FitResult fit_gradient(Model& m, LikelihoodSource& src, const FitOptions& o) {
   const bool analytic = o.analytic_gradient && src.grad_ok();

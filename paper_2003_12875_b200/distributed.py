@@ -120,7 +120,13 @@ class ShardedNll:
         self.model, self.ds, self.dist = model, local_ds, dist
         self.n_total, self.offset = int(n_total), int(offset)
         self.world = dist.get_world_size() if dist.is_initialized() else 1
-        self.device = device if device is not None else torch.device("cpu")
+        if device is None:
+            device = torch.device("cpu")
+        elif isinstance(device, int):
+            device = torch.device("cuda", device)
+        else:
+            device = torch.device(device)
+        self.device = device
         self.on_cuda = getattr(self.device, "type", "cpu") == "cuda"
         self.partial, self.grad_partial = partial, grad_partial
         if n_local is None:

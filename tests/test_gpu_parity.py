@@ -92,14 +92,18 @@ def test_multi_point_launch_parity(w):
 
 
 def test_points_are_independent_of_batching():
-    """A point's value does not depend on the other points of the launch (bitwise)."""
+    """A point's value does not depend on the other points of the launch: bitwise within a
+    kernel (the tile kernel over 40 points or over 9 of them), and to the last bit of the
+    compensated cross-tile sum between kernels (one point: the streaming kernel)."""
     w = configs.C2
     m, ds, _, _ = setup(w.text, 300_001, 7)
     pts = w.points(m, n_points=40)
     full, _, _ = fb.nll_points(m, ds, pts)
-    for p in (0, 13, 39):
+    for p in (0, 13, 31):
+        nine, _, _ = fb.nll_points(m, ds, pts[p:p + 9])
+        assert np.array_equal(nine, full[p:p + 9])
         one, _, _ = fb.nll_points(m, ds, pts[p:p + 1])
-        assert one[0] == full[p]
+        assert abs(one[0] - full[p]) <= 2.5e-16 * abs(full[p])
     again, _, _ = fb.nll_points(m, ds, pts)
     assert np.array_equal(again, full)  # deterministic run to run
 
@@ -784,7 +788,9 @@ def test_plan_specialised_build_matches_static_build(name):
         fb.plan_spec_min_work(old)
     assert np.array_equal(bad, sbad)
     assert np.array_equal(spec, static), np.max(np.abs(spec - static) / np.abs(static))
-    assert np.array_equal(few_spec, few), np.max(np.abs(few_spec - few) / np.abs(few))
+    # few points: the specialised streaming kernel where one exists against the static build
+    # (a different summation tree: equal to the last bit or two of the total)
+    assert np.max(np.abs(few_spec - few) / np.abs(few)) <= 5e-16
     for p in (0, 11):
         _, comp, ob = o.nll(cols, pts[p])
         assert bad[p] == ob
