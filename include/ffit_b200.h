@@ -318,9 +318,11 @@ int ffcu_shard_group_info(const ffcu_shard_group* g, int* world, int* local_devi
 int ffcu_shard_group_nll_points(ffcu_shard_group* g, const double* points, int P, double* values,
                                 long long* first_invalid, unsigned long long* n_evaluations);
 /* Asynchronous on `stream` (groups with one local device): the combined event pairs (2P
- * doubles, no extended term) and global first-invalid indices stay on the device. */
+ * doubles, no extended term) and global first-invalid indices stay on the device;
+ * upload_stream (may be NULL) as in ffcu_nll_points_device_upload. */
 int ffcu_shard_group_nll_points_device(ffcu_shard_group* g, const double* points, int P, double* d_sc,
-                                       unsigned long long* d_bad, void* stream, unsigned long long* n_evaluations);
+                                       unsigned long long* d_bad, void* stream, void* upload_stream,
+                                       unsigned long long* n_evaluations);
 /* ffcu_nll_grad over all ranks: per-rank slot pairs of the fused gradient pass, one
  * all-gather, rank-order combine, host finish with the global event count. */
 int ffcu_shard_group_nll_grad(ffcu_shard_group* g, const double* points, int P, double* values, double* grads,

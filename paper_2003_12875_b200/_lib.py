@@ -131,7 +131,7 @@ SIGNATURES = {
     "ffcu_shard_group_free": (None, [VP]),
     "ffcu_shard_group_info": (I, [VP, IP, IP, LLP, LLP, LLP]),
     "ffcu_shard_group_nll_points": (I, [VP, DP, I, DP, LLP, ULLP]),
-    "ffcu_shard_group_nll_points_device": (I, [VP, DP, I, VP, VP, VP, ULLP]),
+    "ffcu_shard_group_nll_points_device": (I, [VP, DP, I, VP, VP, VP, VP, ULLP]),
     "ffcu_shard_group_nll_grad": (I, [VP, DP, I, DP, DP, LLP, ULLP]),
     "ffcu_shard_group_fit": (I, [VP, D, ctypes.c_long, ctypes.POINTER(VP)]),
     "ffcu_shard_group_fit_gradient": (I, [VP, D, ctypes.c_long, I, ctypes.POINTER(VP)]),

@@ -1112,7 +1112,7 @@ FFB_API int ffcu_shard_group_nll_points(ffcu_shard_group* g, const double* point
 }
 
 FFB_API int ffcu_shard_group_nll_points_device(ffcu_shard_group* g, const double* points, int P, double* d_sc,
-                                               unsigned long long* d_bad, void* stream,
+                                               unsigned long long* d_bad, void* stream, void* upload_stream,
                                                unsigned long long* n_evaluations) {
   return guarded([&] {
     require(g, "group");
@@ -1120,7 +1120,8 @@ FFB_API int ffcu_shard_group_nll_points_device(ffcu_shard_group* g, const double
     require(d_sc, "d_sc");
     require(d_bad, "d_bad");
     const int k = g->g->nll_points_device(points, P, reinterpret_cast<ffb::SumPair*>(d_sc), d_bad,
-                                          static_cast<cudaStream_t>(stream));
+                                          static_cast<cudaStream_t>(stream),
+                                          static_cast<cudaStream_t>(upload_stream));
     if (n_evaluations) *n_evaluations = static_cast<unsigned long long>(k);
   });
 }

@@ -197,7 +197,7 @@ NllResult ShardGroup::nll_points(const double* thetas, int P) {
 }
 
 int ShardGroup::nll_points_device(const double* thetas, int P, SumPair* d_pairs, unsigned long long* d_bad,
-                                  cudaStream_t stream) {
+                                  cudaStream_t stream, cudaStream_t upload_stream) {
   if (local_.size() != 1) usage_error("nll_points_device: one local device per group (create_rank)");
   if (P <= 0) return 0;
   if (P > kMaxPointsPerLaunch) usage_error("nll_points_device: at most 512 points per call");
@@ -207,7 +207,8 @@ int ShardGroup::nll_points_device(const double* thetas, int P, SumPair* d_pairs,
   const std::size_t words = 3 * static_cast<std::size_t>(P);
   ensure_words(L, words, P);
   int launches = L.engine->nll_points_device(*L.ds, thetas, P, reinterpret_cast<SumPair*>(L.d_send),
-                                             reinterpret_cast<unsigned long long*>(L.d_send + 2 * P), s);
+                                             reinterpret_cast<unsigned long long*>(L.d_send + 2 * P), s,
+                                             upload_stream);
   nccl_check(nccl().all_gather(L.d_send, L.d_recv, words, ncclUint64, L.comm, s), "ncclAllGather");
   launches += launch_combine_shards(L.d_recv, world_, P, P, L.d_offsets, d_pairs, d_bad, s);
   count_launches(1);

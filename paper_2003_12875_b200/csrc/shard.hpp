@@ -52,8 +52,9 @@ class ShardGroup : public LikelihoodSource {
 
   // Asynchronous on `stream` (single local device): the combined pairs (events only, no
   // extended term) and global first-invalid indices of P <= 512 points stay on the device.
+  // upload_stream (optional): where the constant rows are copied (a pipeline's copy stream).
   int nll_points_device(const double* thetas, int P, SumPair* d_pairs, unsigned long long* d_bad,
-                        cudaStream_t stream);
+                        cudaStream_t stream, cudaStream_t upload_stream = nullptr);
 
   int world() const { return world_; }
   int local_count() const { return static_cast<int>(local_.size()); }

@@ -742,13 +742,15 @@ class ShardGroup:
                                                  ctypes.byref(ne)))
         return vals, bad, ne.value
 
-    def nll_points_device(self, points, d_sc_ptr, d_bad_ptr, stream_ptr=None) -> int:
+    def nll_points_device(self, points, d_sc_ptr, d_bad_ptr, stream_ptr=None, upload_stream_ptr=None) -> int:
         """Async on a CUDA stream: combined pairs (2P doubles, no extended term) and global
-        first-invalid indices (P uint64) into device buffers."""
+        first-invalid indices (P uint64) into device buffers; upload_stream_ptr: copy the
+        constant rows on that stream (a pipeline's copy stream)."""
         pts = _f64(np.atleast_2d(points))
         ne = ctypes.c_ulonglong()
         _check(lib().ffcu_shard_group_nll_points_device(self._h, _dp(pts), pts.shape[0], VP(d_sc_ptr),
-                                                        VP(d_bad_ptr), VP(stream_ptr or 0), ctypes.byref(ne)))
+                                                        VP(d_bad_ptr), VP(stream_ptr or 0),
+                                                        VP(upload_stream_ptr or 0), ctypes.byref(ne)))
         return ne.value
 
     def nll_grad(self, points):
