@@ -1,12 +1,12 @@
 # A/B of NVRTC build options (plan-specialised builds, FFB_JIT_OPTS) and env knobs on several
 # workloads:  TAG=.. WS="c4 c1" VARIANTS="base: tree:-DFFB_LOG_TREE waves8:env=FFB_NLL_WAVES=8" bash tools/ab_jit.sh
-# (a variant's tokens are comma-separated: -D... go to FFB_JIT_OPTS, env=K=V is exported,
+# (a variant's tokens are '+'-separated: -D... go to FFB_JIT_OPTS, env=K=V is exported,
 #  lib=<tag> loads lib/ab/libffit_b200_<tag>.so)
 TAG=${TAG:-r02jit}; O=gpurun_out/$TAG; mkdir -p $O
 for rep in $(seq 1 ${REPS:-2}); do
   for w in ${WS:-c4}; do
     for v in $VARIANTS; do
-      name=${v%%:*}; toks=$(echo ${v#*:} | tr ',' ' ')
+      name=${v%%:*}; toks=$(echo ${v#*:} | tr '+' ' ')
       opts=""; lib=""; envs=""
       for t in $toks; do
         case $t in lib=*) lib=${t#lib=};; env=*) envs="$envs ${t#env=}";; *) opts="$opts $t";; esac
