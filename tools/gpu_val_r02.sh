@@ -1,0 +1,14 @@
+set -x
+TAG=r02_v10
+O=gpurun_out/$TAG
+mkdir -p $O
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $O/smi.txt
+timeout 1500 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest rc $?" >> $O/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc $?" >> $O/smoke.log
+timeout 600 python bench.py > $O/bench_default.json 2> $O/bench_default.err
+timeout 600 python bench.py --impl reference > $O/bench_reference.json 2> $O/bench_reference.err
+CMD="python bench.py --no-cpu-baseline --steps 2 --warmup 3"
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_c4.csv $CMD > $O/ncu_launch.log 2>&1
+python profiles/summarize.py launches $O/launches_c4.csv > $O/launches_c4.txt 2>&1
+tail -3 $O/pytest_gpu.log $O/smoke.log
+cat $O/bench_default.json
