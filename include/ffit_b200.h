@@ -211,6 +211,21 @@ int ffcu_eval_batch_device(ffit_model* m, const char* pdf, const ffit_dataset* d
 /* normalization(spec, lo, hi, graph) (proj/include/ffit/eval.hpp:26) of a named
  * pdf at a point (NULL = current values). */
 int ffcu_normalization(const ffit_model* m, const char* pdf, const double* point, double* out);
+/* Device-side numeric normalisation (replaces the host's
+ * integrate_adaptive_simpson, proj/src/eval.cpp:40-69, for the nodes without a closed form).
+ * Off by default: the host's quadrature is bit-identical to the reference's.  On (per model, or
+ * FFB_DEVICE_NORM=1 for the process): every likelihood / probabilities / eval_batch call
+ * integrates those nodes on the GPU for all its points at once -- the reference's own adaptive
+ * rule, one warp per point, one lane per pre-panel -- and agrees with the host's value to
+ * <= 1e-13 relative. */
+int ffcu_model_set_device_normalization(ffit_model* m, int on);
+int ffcu_model_device_normalization(const ffit_model* m);
+/* The normalisation integral of a named pdf (NULL = the model's top pdf) at P points (P rows of
+ * all model parameters, declaration order; NULL with P = 1 = current values) by the device
+ * quadrature, whatever the model's switch says; closed forms stay closed forms. */
+int ffcu_device_normalization(ffit_model* m, const char* pdf, const double* points, int P, double* out);
+/* Quadrature kernels this model's engine has launched. */
+unsigned long long ffcu_device_normalization_launches(const ffit_model* m);
 /* The flattened plan and one point's constant row (host logic, no GPU needed). */
 int ffcu_plan_info(const ffit_model* m, int* nterms, int* ncols, int* stride);
 int ffcu_plan_term(const ffit_model* m, int i, int* kind, int* col, int* order, int* flags,
@@ -351,6 +366,9 @@ unsigned long long ffcu_kernel_launches(void);
 int ffcu_math_probe(int which, const double* in, double* out, long long n);
 /* Measured FP64 FMA instructions per second on the current device. */
 int ffcu_fp64_peak(double* fma_per_s, float* ms);
+/* Issue-slot probe: FP64 FMA instructions per second with `others_per_8` (0, 2, 4, 5, 6, 8 or 16)
+ * independent integer multiply-adds issued per eight DFMAs. */
+int ffcu_fp64_issue_probe(int others_per_8, double* fma_per_s);
 /* Seeded generator into host columns (one per observable, each n doubles). */
 int ffcu_sample_host(ffit_model* m, long long n, unsigned long long seed, double* const* cols,
                      double* efficiency);

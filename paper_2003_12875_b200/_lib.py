@@ -82,6 +82,10 @@ SIGNATURES = {
     "ffcu_eval_batch": (I, [VP, CP, VP, DP]),
     "ffcu_eval_batch_device": (I, [VP, CP, VP, VP, VP]),
     "ffcu_normalization": (I, [VP, CP, DP, DP]),
+    "ffcu_model_set_device_normalization": (I, [VP, I]),
+    "ffcu_model_device_normalization": (I, [VP]),
+    "ffcu_device_normalization": (I, [VP, CP, DP, I, DP]),
+    "ffcu_device_normalization_launches": (ULL, [VP]),
     "ffcu_plan_info": (I, [VP, IP, IP, IP]),
     "ffcu_plan_term": (I, [VP, I, IP, IP, IP, IP, IP]),
     "ffcu_point_constants": (I, [VP, DP, DP]),
@@ -119,6 +123,7 @@ SIGNATURES = {
     "ffcu_kernel_timer": (I, [I]),
     "ffcu_kernel_timer_read": (I, [DP, ULLP]),
     "ffcu_fp64_peak": (I, [DP, ctypes.POINTER(ctypes.c_float)]),
+    "ffcu_fp64_issue_probe": (I, [I, DP]),
     "ffcu_math_probe": (I, [I, DP, DP, LL]),
     "ffcu_sample_host": (I, [VP, LL, ULL, ctypes.POINTER(DP), DP]),
     # event-sharded likelihood over several GPUs (csrc/shard.hpp)

@@ -591,6 +591,41 @@ FFB_API int ffcu_normalization(const ffit_model* m, const char* pdf, const doubl
   });
 }
 
+FFB_API int ffcu_model_set_device_normalization(ffit_model* m, int on) {
+  return guarded([&] {
+    require(m, "model");
+    m->engine->set_device_normalization(on != 0);
+  });
+}
+
+FFB_API int ffcu_model_device_normalization(const ffit_model* m) {
+  return m && m->engine && m->engine->device_normalization() ? 1 : 0;
+}
+
+FFB_API int ffcu_device_normalization(ffit_model* m, const char* pdf, const double* points, int P, double* out) {
+  return guarded([&] {
+    require(m, "model");
+    require(out, "out");
+    if (P < 0) ffb::usage_error("negative point count");
+    const int id = pdf ? m->m->pdf_index(pdf) : m->m->root;
+    if (id < 0) ffb::usage_error(std::string("unknown pdf: ") + pdf);
+    if (P == 0) return;
+    std::vector<double> own;
+    if (!points) {
+      if (P != 1) ffb::usage_error("points == NULL needs P == 1 (the model's current values)");
+      own = m->m->theta();
+      points = own.data();
+    }
+    std::vector<double> res(P);  // out stays untouched on failure
+    m->engine->device_normalization_of(id, points, P, res.data());
+    std::copy(res.begin(), res.end(), out);
+  });
+}
+
+FFB_API unsigned long long ffcu_device_normalization_launches(const ffit_model* m) {
+  return m && m->engine ? m->engine->device_norm_launches() : 0ull;
+}
+
 FFB_API int ffcu_plan_info(const ffit_model* m, int* nterms, int* ncols, int* stride) {
   return guarded([&] {
     require(m, "model");
@@ -1250,6 +1285,22 @@ FFB_API int ffcu_math_probe(int which, const double* in, double* out, long long 
     cudaFree(d_in);
     cudaFree(d_out);
     ffb::cuda_check(e, "math_probe");
+  });
+}
+
+FFB_API int ffcu_fp64_issue_probe(int others_per_8, double* fma_per_s) {
+  return guarded([&] {
+    require(fma_per_s, "fma_per_s");
+    if (others_per_8 != 0 && others_per_8 != 2 && others_per_8 != 4 && others_per_8 != 5 && others_per_8 != 6 &&
+        others_per_8 != 8 && others_per_8 != 16) {
+      ffb::usage_error("ffcu_fp64_issue_probe: others_per_8 must be 0, 2, 4, 5, 6, 8 or 16");
+    }
+    cudaStream_t s;
+    ffb::cuda_check(cudaStreamCreate(&s), "cudaStreamCreate");
+    *fma_per_s = ffb::fp64_issue_probe(others_per_8, s);
+    ffb::cuda_check(cudaGetLastError(), "fp64_issue_probe");
+    cudaStreamDestroy(s);
+    ffb::count_launches(2);
   });
 }
 

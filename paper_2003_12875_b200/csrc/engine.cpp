@@ -7,9 +7,11 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <mutex>
+#include <optional>
 #include <sstream>
 #include <utility>
 
@@ -173,7 +175,10 @@ void DeviceDataset::download(int col, double* host_out) const {
 // ---------------------------------------------------------------------------
 // Engine
 
-Engine::Engine(const Model& m) : m_(m), plan_(compile_plan(m, m.root, true)) {}
+Engine::Engine(const Model& m) : m_(m), plan_(compile_plan(m, m.root, true)) {
+  const char* e = std::getenv("FFB_DEVICE_NORM");
+  device_norm_ = e != nullptr && e[0] == '1';
+}
 
 Engine::~Engine() {
   if (device_ >= 0) {
@@ -195,6 +200,11 @@ Engine::~Engine() {
     cudaFree(d_gslots_);
     cudaFreeHost(h_gslots_);
     cudaFree(d_prog_);
+    cudaFree(d_nrows_);
+    cudaFree(d_nout_);
+    cudaFree(d_nstatus_);
+    for (auto& j : norm_jobs_) cudaFree(j.second.d_prog);
+    if (norm_stream_) cudaStreamDestroy(norm_stream_);
     if (stream_) cudaStreamDestroy(stream_);
     cudaSetDevice(prev);
   }
@@ -287,6 +297,104 @@ const double* Engine::copy_rows(const HostPlan& plan, int k, int P, cudaStream_t
   return d_consts_[k];
 }
 
+bool Engine::device_norms(int pdf, const double* thetas, int P) {
+  if (!device_norm_ || device_ < 0 || P <= 0) return false;
+  const int npar = static_cast<int>(m_.params.size());
+  const int npdf = static_cast<int>(m_.pdfs.size());
+  // which nodes take the Simpson route is decided at the first point (it depends on the
+  // parameters only through ArgusBG's p == 1/2); a node that needs a quadrature at a later
+  // point only falls back to the host's
+  const std::vector<int> nodes = m_.simpson_nodes(pdf, thetas);
+  if (nodes.empty()) return false;
+  norm_cache_.assign(static_cast<std::size_t>(P) * npdf, std::numeric_limits<double>::quiet_NaN());
+  if (!norm_stream_) cuda_check(cudaStreamCreateWithFlags(&norm_stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+  if (P > cap_nout_) {
+    cudaFree(d_nout_);
+    cudaFree(d_nstatus_);
+    cap_nout_ = std::max(P, 64);
+    cuda_check(cudaMalloc(&d_nout_, cap_nout_ * sizeof(double)), "cudaMalloc(norms)");
+    cuda_check(cudaMalloc(&d_nstatus_, cap_nout_ * sizeof(int)), "cudaMalloc(norm status)");
+  }
+  std::vector<double> rows, vals(P);
+  std::vector<int> status(P);
+  for (const int id : nodes) {  // children before parents
+    auto it = norm_jobs_.find(id);
+    if (it == norm_jobs_.end()) {
+      NormJob job;
+      job.plan = compile_plan(m_, id, false);
+      if (!job.plan.programs.empty()) {
+        const std::size_t bytes = job.plan.programs.size() * sizeof(ExprInstr);
+        cuda_check(cudaMalloc(&job.d_prog, bytes), "cudaMalloc(programs)");
+        cuda_check(cudaMemcpy(job.d_prog, job.plan.programs.data(), bytes, cudaMemcpyHostToDevice),
+                   "cudaMemcpy(programs)");
+        job.plan.dev.prog = job.d_prog;
+      }
+      it = norm_jobs_.emplace(id, std::move(job)).first;
+    }
+    const HostPlan& plan = it->second.plan;
+    const int stride = std::max(1, plan.dev.stride);
+    rows.assign(static_cast<std::size_t>(P) * stride, 0.0);
+    // the sub-pdf's unnormalised rows: its children's normalisations are already in the cache
+    for (int p = 0; p < P; ++p) {
+      NormOverride ov(&norm_cache_[static_cast<std::size_t>(p) * npdf]);
+      build_constants(plan, m_, thetas + static_cast<std::size_t>(p) * npar, &rows[static_cast<std::size_t>(p) * stride],
+                      1.0);
+    }
+    if (rows.size() > cap_nrows_) {
+      cudaFree(d_nrows_);
+      cap_nrows_ = rows.size();
+      cuda_check(cudaMalloc(&d_nrows_, cap_nrows_ * sizeof(double)), "cudaMalloc(norm rows)");
+    }
+    cuda_check(cudaMemcpyAsync(d_nrows_, rows.data(), rows.size() * sizeof(double), cudaMemcpyHostToDevice, norm_stream_),
+               "cudaMemcpyAsync(norm rows)");
+    const Observable& o = m_.obs_of(id);
+    const int launches = launch_simpson(plan.dev, d_nrows_, P, o.lo, o.hi, 1e-10 * (o.hi - o.lo), 1e-10, 60, d_nout_,
+                                        d_nstatus_, norm_stream_);
+    cuda_check(cudaGetLastError(), "launch_simpson");
+    cuda_check(cudaMemcpyAsync(vals.data(), d_nout_, P * sizeof(double), cudaMemcpyDeviceToHost, norm_stream_),
+               "cudaMemcpyAsync(norms)");
+    cuda_check(cudaMemcpyAsync(status.data(), d_nstatus_, P * sizeof(int), cudaMemcpyDeviceToHost, norm_stream_),
+               "cudaMemcpyAsync(norm status)");
+    cuda_check(cudaStreamSynchronize(norm_stream_), "device normalisation");
+    count_launches(launches);
+    norm_launches_ += launches;
+    for (int p = 0; p < P; ++p) {
+      if (status[p]) numeric_error("non-finite integrand in the normalisation of '" + m_.pdfs[id].name + "'");
+      norm_cache_[static_cast<std::size_t>(p) * npdf + id] = vals[p];
+    }
+  }
+  return true;
+}
+
+void Engine::device_normalization_of(int pdf, const double* thetas, int P, double* out) {
+  if (P <= 0) return;
+  int dev = device_;
+  if (dev < 0) cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  DeviceGuard g(dev);
+  ensure(dev, 1, 0);
+  const int npar = static_cast<int>(m_.params.size());
+  const int npdf = static_cast<int>(m_.pdfs.size());
+  for (int p = 0; p < P; ++p) m_.check_params(pdf, thetas + static_cast<std::size_t>(p) * npar);
+  const bool was = device_norm_;
+  device_norm_ = true;
+  bool have = false;
+  try {
+    have = device_norms(pdf, thetas, P);
+  } catch (...) {
+    device_norm_ = was;
+    throw;
+  }
+  device_norm_ = was;
+  for (int p = 0; p < P; ++p) {
+    if (have) {
+      NormOverride ov(&norm_cache_[static_cast<std::size_t>(p) * npdf]);
+      out[p] = m_.normalization(pdf, thetas + static_cast<std::size_t>(p) * npar);
+    } else {
+      out[p] = m_.normalization(pdf, thetas + static_cast<std::size_t>(p) * npar);
+    }
+  }
+}
+
 int Engine::build_rows(const HostPlan& plan, const double* thetas, int P, double extra_scale) {
   const int k = slot_ ^= 1;
   // slot k fed the copy two calls ago; that copy must be done before reuse
@@ -297,7 +405,13 @@ int Engine::build_rows(const HostPlan& plan, const double* thetas, int P, double
   // rows are expensive (Simpson normalisations: Expression / ChiSquare / JohnsonSU), else
   // build them here -- analytic rows take ~0.2-1 us, less than waking the pool (each row
   // is validated; the first invalid point's error is raised)
+  // (device-side numeric normalisation, when on: the Simpson-normalised nodes of all P points
+  // first, in a few launches; the rows then read those values)
+  const bool dn = device_norms(plan.pdf, thetas, P);
+  const int npdf = static_cast<int>(m_.pdfs.size());
   auto row = [&](int p) {
+    std::optional<NormOverride> ov;
+    if (dn) ov.emplace(&norm_cache_[static_cast<std::size_t>(p) * npdf]);
     build_constants(plan, m_, thetas + static_cast<std::size_t>(p) * npar,
                     h_consts_[k] + static_cast<std::size_t>(p) * stride, extra_scale);
   };
@@ -479,7 +593,11 @@ NllResult Engine::nll_points_graph(const DeviceDataset& ds, const double* thetas
   // rows into slot 0 (any earlier asynchronous copy out of it has completed)
   cuda_check(cudaEventSynchronize(staged_[0]), "cudaEventSynchronize");
   const int stride = plan_.dev.stride;
+  const bool dn = device_norms(plan_.pdf, thetas, P);  // (the quadrature stays outside the graph)
+  const int npdf = static_cast<int>(m_.pdfs.size());
   for (int p = 0; p < P; ++p) {
+    std::optional<NormOverride> ov;
+    if (dn) ov.emplace(&norm_cache_[static_cast<std::size_t>(p) * npdf]);
     build_constants(plan_, m_, thetas + static_cast<std::size_t>(p) * npar,
                     h_consts_[0] + static_cast<std::size_t>(p) * stride, std::ldexp(1.0, kPScaleLog2));
   }

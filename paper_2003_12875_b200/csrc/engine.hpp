@@ -7,6 +7,7 @@
 
 #include <cuda_runtime.h>
 
+#include <map>
 #include <memory>
 #include <string>
 #include <vector>
@@ -124,6 +125,20 @@ class Engine {
   void eval_batch(int pdf, const DeviceDataset& ds, const double* theta, double* out,
                   bool out_on_device, cudaStream_t stream = nullptr);
 
+  // Device-side numeric normalisation.  Off (the default): every Simpson
+  // normalisation is the host's, bit-identical to the reference's.  On: the nodes of a launch's
+  // plan whose normalisation has no closed form (Expression, ChiSquare, JohnsonSU, ArgusBG with
+  // p != 1/2, sums over them) are integrated on the GPU for all P points at once -- the
+  // reference's own adaptive rule, one warp per point (kernels_device.cuh simpson_kernel) --
+  // and the host builds the constant rows from those values.  FFB_DEVICE_NORM=1 switches it
+  // on for every engine.
+  void set_device_normalization(bool on) { device_norm_ = on; }
+  bool device_normalization() const { return device_norm_; }
+  // The normalisation integral of `pdf` at P points by the device quadrature (children's
+  // normalisations included, bottom-up); out[P].  On the current device (or the engine's).
+  void device_normalization_of(int pdf, const double* thetas, int P, double* out);
+  unsigned long long device_norm_launches() const { return norm_launches_; }
+
   const HostPlan& likelihood_plan() const { return plan_; }
   NllLaunchInfo last_launch() const { return last_; }
   cudaStream_t stream(int device);
@@ -153,6 +168,24 @@ class Engine {
   void ensure(int device, int P, std::size_t scratch);
   const double* upload_constants(const HostPlan& plan, const double* thetas, int P, cudaStream_t s,
                                  double extra_scale = 1.0);
+
+  // fills norm_cache_ (P x pdfs, NaN = not computed) for the Simpson-normalised nodes under
+  // `pdf`; false when there are none (or the device path is off)
+  bool device_norms(int pdf, const double* thetas, int P);
+  struct NormJob {
+    HostPlan plan;
+    ExprInstr* d_prog = nullptr;
+  };
+  std::map<int, NormJob> norm_jobs_;
+  std::vector<double> norm_cache_;
+  bool device_norm_ = false;
+  cudaStream_t norm_stream_ = nullptr;
+  double* d_nrows_ = nullptr;
+  double* d_nout_ = nullptr;
+  int* d_nstatus_ = nullptr;
+  std::size_t cap_nrows_ = 0;
+  int cap_nout_ = 0;
+  unsigned long long norm_launches_ = 0;
 
   const Model& m_;
   HostPlan plan_;

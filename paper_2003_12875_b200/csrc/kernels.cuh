@@ -97,6 +97,12 @@ int launch_math_probe(int which, const double* d_in, double* d_out, long long n,
 
 // DFMA-chain microbenchmark: returns FP64 FMA instructions per second measured
 // with CUDA events on `stream` (the FP64 roofline denominator).
+// Device-side numeric normalisation: the reference's adaptive Simpson of `plan` (an unnormalised
+// sub-pdf plan, one row of constants per point) over [lo, hi] for P points; d_out[p] = integral,
+// d_status[p] != 0 where the integrand was not finite.  Returns the launch count.
+int launch_simpson(const DevPlan& plan, const double* d_rows, int P, double lo, double hi, double abs_tol,
+                   double rel_tol, int max_depth, double* d_out, int* d_status, cudaStream_t stream);
 double fp64_peak(cudaStream_t stream, float* ms_out);
+double fp64_issue_probe(int others, cudaStream_t stream);
 
 }  // namespace ffb

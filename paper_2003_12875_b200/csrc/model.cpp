@@ -637,10 +637,34 @@ double Model::simpson_integral(int id, const double* theta) const {
   return integrate_adaptive_simpson(f, o.lo, o.hi, 1e-10 * (o.hi - o.lo), 1e-10, 60);
 }
 
+namespace {
+thread_local const double* tl_norm_override = nullptr;
+}
+
+NormOverride::NormOverride(const double* values) : prev_(tl_norm_override) { tl_norm_override = values; }
+NormOverride::~NormOverride() { tl_norm_override = prev_; }
+
+std::vector<int> Model::simpson_nodes(int id, const double* theta) const {
+  std::vector<int> out;
+  std::function<void(int)> walk = [&](int n) {
+    const Pdf& p = pdfs[n];
+    for (const int c : p.children) walk(c);
+    if (p.kind == Kind::ProdPdf || p.obs < 0) return;
+    const Observable& o = observables[p.obs];
+    if (!analytic_integral(n, o.lo, o.hi, theta) && std::find(out.begin(), out.end(), n) == out.end()) {
+      out.push_back(n);
+    }
+  };
+  walk(id);
+  return out;
+}
+
 double Model::normalization(int id, const double* theta) const {
   const Pdf& p = pdfs[id];
   double r;
-  if (p.kind == Kind::ProdPdf) {
+  if (tl_norm_override && !std::isnan(tl_norm_override[id])) {
+    r = tl_norm_override[id];
+  } else if (p.kind == Kind::ProdPdf) {
     r = 1.0;
     for (const int c : p.children) r *= normalization(c, theta);
   } else if (p.obs < 0) {

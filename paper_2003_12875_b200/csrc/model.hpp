@@ -93,6 +93,10 @@ class Model {
   std::optional<double> analytic_integral(int pdf, double lo, double hi,
                                           const double* theta) const;
   double simpson_integral(int pdf, const double* theta) const;
+  // The 1-D nodes under `pdf` whose normalization() takes the Simpson route at theta (no
+  // closed form), children before parents: what the device quadrature computes
+  // (Engine::device_norms).
+  std::vector<int> simpson_nodes(int pdf, const double* theta) const;
 
   // Unnormalised density at one point of a 1-D subtree (PdfSpec::eval_unnorm,
   // proj/src/pdfs.cpp:178-210).  Used for Simpson normalisation and the toy
@@ -114,6 +118,20 @@ class Model {
 
   // Observable range of a 1-D subtree.
   const Observable& obs_of(int pdf) const { return observables[pdfs[pdf].obs]; }
+};
+
+// While alive on this thread, normalization(id, .) returns values[id] wherever it is not NaN
+// (one entry per pdf): normalisations computed elsewhere -- the device quadrature -- for the
+// parameter point being built.  The degenerate-value check still applies.
+class NormOverride {
+ public:
+  explicit NormOverride(const double* values);
+  ~NormOverride();
+  NormOverride(const NormOverride&) = delete;
+  NormOverride& operator=(const NormOverride&) = delete;
+
+ private:
+  const double* prev_;
 };
 
 // Adaptive Simpson with 32 pre-panels (proj/src/eval.cpp:14-69).

@@ -442,6 +442,35 @@ def normalization(model: Model, pdf: str | None = None, point=None) -> float:
     return out.value
 
 
+def set_device_normalization(model: Model, on: bool = True) -> None:
+    """Device-side numeric normalisation for this model's likelihood / probabilities /
+    eval_batch calls (ffcu_model_set_device_normalization; off = the host's adaptive Simpson,
+    bit-identical to the reference's)."""
+    _check(lib().ffcu_model_set_device_normalization(model.handle, 1 if on else 0))
+
+
+def device_normalization_enabled(model: Model) -> bool:
+    return bool(lib().ffcu_model_device_normalization(model.handle))
+
+
+def device_normalization(model: Model, pdf: str | None = None, points=None) -> np.ndarray:
+    """The normalisation integral of a (sub-)pdf at P points by the device quadrature (the
+    reference's adaptive Simpson, one warp per point); points = None: the current values."""
+    if points is None:
+        out = np.empty(1, dtype=np.float64)
+        _check(lib().ffcu_device_normalization(model.handle, None if pdf is None else pdf.encode(), None, 1, _dp(out)))
+        return out
+    pts = _f64(np.atleast_2d(points))
+    out = np.empty(pts.shape[0], dtype=np.float64)
+    _check(lib().ffcu_device_normalization(model.handle, None if pdf is None else pdf.encode(), _dp(pts), pts.shape[0],
+                                           _dp(out)))
+    return out
+
+
+def device_normalization_launches(model: Model) -> int:
+    return int(lib().ffcu_device_normalization_launches(model.handle))
+
+
 @dataclass
 class FittedParameter:
     name: str
@@ -533,6 +562,13 @@ def fp64_peak():
     ms = ctypes.c_float()
     _check(lib().ffcu_fp64_peak(ctypes.byref(v), ctypes.byref(ms)))
     return v.value, ms.value
+
+
+def fp64_issue_probe(others_per_8: int) -> float:
+    """FP64 FMA instructions/s with `others_per_8` integer multiply-adds issued per eight DFMAs."""
+    v = ctypes.c_double()
+    _check(lib().ffcu_fp64_issue_probe(int(others_per_8), ctypes.byref(v)))
+    return v.value
 
 
 def math_probe(which: str, x) -> np.ndarray:
