@@ -488,6 +488,23 @@ def run_ours(args, w):
                          "frac_note": "achieved = FP64-pipe thread instructions the kernel executes per event-point "
                                       "(ncu, profiles/ncu_summary.json) x event-points / kernel time; frac is the "
                                       "FP64 pipe's share of its measured peak"})
+        # the SM's issue limit for this instruction mix: the DFMA rate of a
+        # synthetic stream with the kernel's ratio of non-FP64 instructions (integer multiply-adds),
+        # measured live at the two neighbouring ratios and interpolated
+        total = profiled(w.name, "thread_instr_per_event_point")
+        if total and total > executed:
+            k8 = 8.0 * (total - executed) / executed
+            grid = [0, 2, 4, 5, 6, 8, 16]
+            lo = max(g for g in grid if g <= min(k8, 16))
+            hi = min(g for g in grid if g >= min(k8, 16))
+            r_lo = max(fb.fp64_issue_probe(lo) for _ in range(2)) / 1e12
+            r_hi = r_lo if hi == lo else max(fb.fp64_issue_probe(hi) for _ in range(2)) / 1e12
+            ceil = r_lo if hi == lo else r_lo + (r_hi - r_lo) * (min(k8, 16) - lo) / (hi - lo)
+            roofline["issue_mix"] = {
+                "other_instr_per_8_fp64": k8, "probe_dfma_rate": ceil, "unit": "T fp64-instr/s",
+                "achieved_over_probe": ach / ceil,
+                "note": "DFMA rate of dfma_mix_kernel (8 DFMA chains + K independent IMADs per round) at the "
+                        "kernel's K: what the SM issues at this FP64 : other ratio with nothing else in the way"}
     else:
         roofline.update({"achieved": ach_alg, "frac": ach_alg / peak, "executed_frac": None,
                          "frac_note": "no executed-instruction count profiled for this workload: achieved is the "

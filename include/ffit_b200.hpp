@@ -202,6 +202,11 @@ class Model {
   PdfSpec pdf() { return PdfSpec(*this, ffcu_model_pdf_name(h_.get(), ffcu_model_pdf_count(h_.get()) - 1)); }
   PdfSpec pdf(const std::string& name) { return PdfSpec(*this, name); }
 
+  // numeric normalisations (pdfs without a closed-form integral) by the device quadrature for
+  // this model's likelihood / probabilities / eval_batch calls (off: the host's, as the reference)
+  void set_device_normalization(bool on) { detail::check(ffcu_model_set_device_normalization(h_.get(), on ? 1 : 0)); }
+  bool device_normalization() const { return ffcu_model_device_normalization(h_.get()) != 0; }
+
   ffit_model* handle() const { return h_.get(); }
 
  private:
@@ -234,6 +239,13 @@ inline void PdfSpec::eval_batch(const DataSet& ds, std::span<double> out, std::u
 inline double normalization(const Model& m, const std::string& pdf) {
   double v = 0.0;
   detail::check(ffcu_normalization(m.handle(), pdf.c_str(), nullptr, &v));
+  return v;
+}
+
+// the same integral by the device quadrature (simpson_kernel; closed forms stay closed forms)
+inline double device_normalization(const Model& m, const std::string& pdf) {
+  double v = 0.0;
+  detail::check(ffcu_device_normalization(m.handle(), pdf.c_str(), nullptr, 1, &v));
   return v;
 }
 

@@ -74,6 +74,24 @@ int main() {
   }
   CHECK(threw);
 
+  // a pdf without a closed-form integral: the device quadrature against the host's, and the
+  // likelihood with the model's switch on
+  {
+    auto q = ffit::Model::from_string("observable x 0.1 15\nparameter k 3.5 0.5 20\npdf q ChiSquare(x, k)\n");
+    const double host_norm = ffit::normalization(*q, "q");
+    const double dev_norm = ffit::device_normalization(*q, "q");
+    CHECK(std::fabs(dev_norm - host_norm) <= 1e-13 * host_norm);
+    std::vector<double> qx;
+    for (int i = 0; i < 5001; ++i) qx.push_back(0.2 + 14.0 * i / 5000.0);
+    const ffit::DataSet qd({"x"}, {qx});
+    const double host_nll = ffit::nll(*q, qd, ffit::EvalMode::Gpu).value;
+    CHECK(!q->device_normalization());
+    q->set_device_normalization(true);
+    CHECK(q->device_normalization());
+    const double dev_nll = ffit::nll(*q, qd, ffit::EvalMode::Gpu).value;
+    CHECK(std::fabs(dev_nll - host_nll) <= 1e-13 * std::fabs(host_nll));
+  }
+
   model->set("mu", 0.0);
   ffit::FitOptions o;
   o.tolerance = 1e-10;

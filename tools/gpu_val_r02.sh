@@ -1,5 +1,5 @@
 set -x
-TAG=r02_v10
+TAG=${TAG:-r02_v11}
 O=gpurun_out/$TAG
 mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $O/smi.txt
