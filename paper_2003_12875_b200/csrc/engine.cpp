@@ -321,7 +321,13 @@ bool Engine::device_norms(int pdf, const double* thetas, int P) {
     auto it = norm_jobs_.find(id);
     if (it == norm_jobs_.end()) {
       NormJob job;
-      job.plan = compile_plan(m_, id, false);
+      try {
+        job.plan = compile_plan(m_, id, false);
+      } catch (const Error&) {
+        // a subtree outside the plan's canonical form: its quadrature stays on the host (the
+        // cache keeps NaN for it, so normalization() integrates it as before)
+        job.plan.pdf = -1;
+      }
       if (!job.plan.programs.empty()) {
         const std::size_t bytes = job.plan.programs.size() * sizeof(ExprInstr);
         cuda_check(cudaMalloc(&job.d_prog, bytes), "cudaMalloc(programs)");
@@ -332,6 +338,7 @@ bool Engine::device_norms(int pdf, const double* thetas, int P) {
       it = norm_jobs_.emplace(id, std::move(job)).first;
     }
     const HostPlan& plan = it->second.plan;
+    if (plan.pdf < 0) continue;
     const int stride = std::max(1, plan.dev.stride);
     rows.assign(static_cast<std::size_t>(P) * stride, 0.0);
     // the sub-pdf's unnormalised rows: its children's normalisations are already in the cache
