@@ -851,7 +851,7 @@ void Engine::eval_batch(int pdf, const DeviceDataset& ds, const double* theta, d
     cuda_check(cudaMalloc(&d_out, static_cast<std::size_t>(ds.n) * sizeof(double)), "cudaMalloc(out)");
   }
   const int slot = slot_;  // upload_constants filled this slot
-  count_launches(launch_eval(plan.dev, cols, ds.n, d_consts, d_out, s));
+  count_launches(launch_eval(plan.dev, cols, ds.n, d_consts, d_out, s, h_consts_[slot]));
   cuda_check(cudaGetLastError(), "launch_eval");
   mark_consumed(slot, s);  // a later copy into this slot (any stream) waits for the kernel
   if (!out_on_device) {

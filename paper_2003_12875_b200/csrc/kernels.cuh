@@ -66,8 +66,10 @@ int cache_launch_constants(DevPlan& plan, double* host_consts, int P);
 
 // Per-event values of the plan for one point (probabilities() when the plan is
 // normalised, PdfSpec::eval_batch when not).
+// h_row (the point's constant row on the host) selects the build per leaf-kind set; without it
+// the generic kernel runs.
 int launch_eval(const DevPlan& plan, const ColPtrs& cols, long long n, const double* d_consts,
-                double* d_out, cudaStream_t stream);
+                double* d_out, cudaStream_t stream, const double* h_row = nullptr);
 
 // Combine R per-rank Neumaier pairs per point in fixed rank order (multi-GPU
 // exchange step after an all-gather): in = R x P pairs, out = P pairs.
