@@ -369,6 +369,33 @@ pdf model AddPdf(sig, f, bkg)
     assert abs(fb.nll(m, ds).value - o.nll(cols)[1]) <= NLL_TOL * abs(o.nll(cols)[1])
 
 
+@pytest.mark.parametrize("ncols", [1, 2, 3, 4, 5])
+def test_probabilities_and_eval_batch_over_one_to_five_columns(ncols):
+    """probabilities / eval_batch: the per-kind-set kernel with the columns in registers (up to
+    three columns) and the generic kernel (more) against the oracle, ragged sizes and non-finite
+    data included (proj/src/eval.cpp:174-192, proj/src/pdfs.cpp:212-269)."""
+    names = ["x", "y", "z", "u", "v"][:ncols]
+    lines = [f"observable {n} -4 4" for n in names]
+    lines += [f"parameter m{i} {0.1 * (i + 1)} -1 1\nparameter s{i} {0.8 + 0.1 * i} 0.2 3" for i in range(ncols)]
+    lines += [f"pdf g{i} Gaussian({n}, m{i}, s{i})" for i, n in enumerate(names)]
+    lines += ["pdf model ProdPdf(" + ", ".join(f"g{i}" for i in range(ncols)) + ")"] if ncols > 1 else []
+    text = "\n".join(lines) + "\n"
+    m = fb.Model.from_string(text)
+    o = OracleModel(text)
+    rng = np.random.default_rng(40 + ncols)
+    for n in (1, 2047, 2049, 30_011):
+        cols = [rng.uniform(-4, 4, n) for _ in names]
+        ds = fb.DataSet.from_columns(dict(zip(names, cols)))
+        assert rel(fb.probabilities(m, ds), o.probabilities(cols)) <= PER_EVENT
+        got = fb.eval_batch(m, "g0", ds)  # a one-column sub-pdf of the same dataset
+        assert rel(got, np.exp(-0.5 * ((cols[0] - 0.1) / 0.8) ** 2)) <= PER_EVENT
+    cols = [rng.uniform(-4, 4, 5000) for _ in names]
+    cols[-1][17] = np.nan
+    cols[0][4021] = np.inf
+    p = fb.probabilities(m, fb.DataSet.from_columns(dict(zip(names, cols))))
+    assert np.isnan(p[17]) and np.isnan(p[4021]) and np.all(np.isfinite(np.delete(p, [17, 4021])))
+
+
 def test_product_whose_first_factor_is_a_sum():
     """ProdPdf(AddPdf(a, f, b) on x, Gaussian on y, AddPdf on z): multi-term sums as the
     first and the last factor of a product."""
