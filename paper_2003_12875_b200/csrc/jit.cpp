@@ -1055,17 +1055,6 @@ const SpecTile& spec_tile() {
   return t;
 }
 
-// FFB_EXP_BIG=1: the plan-specialised likelihood builds use the 3211-entry exp table in front of
-// their dynamic shared memory (fastmath.cuh)
-bool exp_big() {
-  static const bool on = [] {
-    const char* v = std::getenv("FFB_EXP_BIG");
-    return v != nullptr && v[0] == '1';
-  }();
-  return on;
-}
-std::size_t exp_front_bytes() { return exp_big() ? kExpBigDoubles * sizeof(double) : 0; }
-
 std::string plan_spec_kernel_name(const DevPlan& d, int ks) {
   return "&ffb::nll_kernel<" + std::to_string(kJitThreads) + ", " + std::to_string(spec_tile().e) + ", " +
          (d.ncols == 1 ? "true" : "false") + ", " + std::to_string(spec_tile().minb) + ", " +
@@ -1094,12 +1083,11 @@ PlanModule* plan_module(const DevPlan& d, int ks) {
         (names.size() < 2 || drv.get_function(&m.stream, m.mod, lowered[1].c_str()) == CUDA_SUCCESS)) {
       const int st = kJitThreads * spec_tile().e;
       drv.set_attribute(m.fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
-                        kMaxCols * st * static_cast<int>(sizeof(double)) + static_cast<int>(exp_front_bytes()));
-      drv.occupancy(&m.occ, m.fn, kJitThreads, (d.ncols + d.ncached) * st * sizeof(double) + exp_front_bytes());
+                        kMaxCols * st * static_cast<int>(sizeof(double)));
+      drv.occupancy(&m.occ, m.fn, kJitThreads, (d.ncols + d.ncached) * st * sizeof(double));
       if (m.occ < 1) m.occ = 1;
       if (m.stream) {
-        const int ss = spec_stream_stages(d) * d.ncols * kJitTile * static_cast<int>(sizeof(double)) +
-                       static_cast<int>(exp_front_bytes());
+        const int ss = spec_stream_stages(d) * d.ncols * kJitTile * static_cast<int>(sizeof(double));
         drv.set_attribute(m.stream, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, ss);
         drv.occupancy(&m.stream_occ, m.stream, kJitThreads, ss);
         if (m.stream_occ < 1) m.stream_occ = 1;
@@ -1147,7 +1135,7 @@ std::string plan_spec_source(const DevPlan& d) {
   // instead of 64-bit immediates materialised per use (A/B, profiles/r01_ab1: +0.2-2.3 %
   // on C2-C4, -0.5 % on C1)
   return "// generated by jit.cpp: the launch's term list for nll_kernel<..., PlanSpec>\n"
-         "#define FFB_CONST_BANK 1\n#define FFB_NLL_ITEM_LOOP 1\n" + std::string(exp_big() ? "#define FFB_EXP_BIG 1\n" : "") +
+         "#define FFB_CONST_BANK 1\n#define FFB_NLL_ITEM_LOOP 1\n" +
          plan_spec_struct(d) + "#include \"kernels_device.cuh\"\n";
 }
 
@@ -1211,8 +1199,7 @@ NllLaunchInfo launch_nll_spec(const DevPlan& launch, const ColPtrs& cols, long l
     void* sargs[] = {&dp, &cp, &nn, &kc, &PP, &ntiles, &partial, &bad};
     if (ev_start) cudaEventRecord(ev_start, stream);
     const CUresult rc = drv.launch(m->stream, static_cast<unsigned>(G), 1, 1, kJitThreads, 1, 1,
-                                   spec_stream_stages(launch) * launch.ncols * kJitTile * sizeof(double) +
-                                       exp_front_bytes(),
+                                   spec_stream_stages(launch) * launch.ncols * kJitTile * sizeof(double),
                                    reinterpret_cast<CUstream>(stream), sargs, nullptr);
     if (ev_stop) cudaEventRecord(ev_stop, stream);
     if (rc != CUDA_SUCCESS) numeric_error("cuLaunchKernel (plan-specialised likelihood) failed: " + std::to_string(rc));
@@ -1243,7 +1230,7 @@ NllLaunchInfo launch_nll_spec(const DevPlan& launch, const ColPtrs& cols, long l
   const long long grid = nll_grid(static_cast<long long>(ntiles) * nchunks, slots);
   const CUresult rc =
       drv.launch(m->fn, static_cast<unsigned>(grid), 1, 1, kJitThreads, 1, 1,
-                 (launch.ncols + launch.ncached) * stile * sizeof(double) + exp_front_bytes(),
+                 (launch.ncols + launch.ncached) * stile * sizeof(double),
                  reinterpret_cast<CUstream>(stream), args, nullptr);
   if (ev_stop) cudaEventRecord(ev_stop, stream);
   if (rc != CUDA_SUCCESS) numeric_error("cuLaunchKernel (plan-specialised likelihood) failed: " + std::to_string(rc));

@@ -27,11 +27,6 @@ constexpr int kMaxTerms = 32;
 constexpr int kPScaleLog2 = 54;
 constexpr int kMaxCols = 8;
 constexpr int kMaxOrder = 12;
-// The 3211-entry exp table of the FFB_EXP_BIG builds (fastmath.cuh, gen_tables.py): entries
-// j = -kExpBigMargin .. ; kExpBigDoubles doubles at the front of the CTA's dynamic shared memory.
-constexpr int kExpBigN = 3211;
-constexpr int kExpBigMargin = 8;
-constexpr int kExpBigDoubles = 3232;
 
 enum LeafKind : int {
   LK_GAUSS = 0,    // c: [coef, mu, -1/(2 sigma^2)]

@@ -1,4 +1,4 @@
-# ncu --set full of the fused kernel under env variants: TAG=.. WS="c4" VARS="base: big:FFB_EXP_BIG=1" bash tools/prof_ab.sh
+# ncu --set full of the fused kernel under env variants: TAG=.. WS="c4" VARS="base: nopre:FFB_JIT_OPTS=-DFFB_EXP_NO_PRESCALE" bash tools/prof_ab.sh
 TAG=${TAG:-r02_prof}; O=gpurun_out/$TAG; mkdir -p $O
 for w in ${WS:-c4}; do
   for v in $VARS; do
