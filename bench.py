@@ -539,11 +539,44 @@ def cpu_baseline(w, cols, pts):
     mat = r.matrix(scalar=w.name == configs.C1.name)
     head = next(c for c in mat["cells"] if c["build"] == "release" and c["mode"] == "BatchPrecise"
                 and c["threads"] == mat["nproc"])
-    return {"value": head["value"], "unit": UNIT, "cores": mat["nproc"], "kind": "reference",
-            "sample": f"{head['points']} points (one per thread) x the first {head['events']} of this rank's events "
-                      f"per call, median of 7; oracle/_ref = the unmodified reference engine, Release flags, "
-                      f"BatchPrecise, {r.arm.note}",
-            "matrix": mat}
+    out = {"value": head["value"], "unit": UNIT, "cores": mat["nproc"], "kind": "reference",
+           "sample": f"{head['points']} points (one per thread) x the first {head['events']} of this rank's events "
+                     f"per call, median of 7; oracle/_ref = the unmodified reference engine, Release flags, "
+                     f"BatchPrecise, {r.arm.note}",
+           "matrix": mat}
+    out["port"] = cpu_port(w, cols, pts, mat["nproc"] or 1)
+    return out
+
+
+def cpu_port(w, cols, pts, threads):
+    """the restated oracle (oracle/ffit_oracle.c, the workload's NATIVE kinds --
+    ArgusBG, Chebychev, ProdPdf, the extended term -- in one model, one point per thread) timed
+    beside the reference engine's spelling: 1 thread and all threads, median of 5 on a bounded
+    sample."""
+    import numpy as np
+
+    from oracle import oracle as orc
+    o = orc.OracleModel(w.text)
+    xs = [np.ascontiguousarray(cols[name]) for (name, _, _) in o.obs]
+    n_full = len(xs[0])
+
+    def call(nsub, npts, nthreads):
+        sub = [x[:nsub] for x in xs]
+        th = np.ascontiguousarray(pts[[i % len(pts) for i in range(npts)]])
+        t0 = time.perf_counter()
+        o.nll_points(sub, th, nthreads)
+        return time.perf_counter() - t0
+
+    cells = []
+    for nthreads in sorted({1, threads}):
+        probe = min(n_full, 100_000)
+        per = max(call(probe, nthreads, nthreads), 1e-6) / probe
+        nsub = int(min(n_full, max(probe, 0.12 / per)))
+        med = sorted(call(nsub, nthreads, nthreads) for _ in range(5))[2]
+        cells.append({"threads": nthreads, "value": nsub * nthreads / med, "unit": UNIT, "events": nsub,
+                      "points": nthreads, "median_s": med})
+    return {"kind": "port", "what": "oracle/ffit_oracle.c (C restatement, -O2, scalar per event; native kinds)",
+            "cells": cells}
 
 
 # ---------------------------------------------------------------------------
