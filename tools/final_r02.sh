@@ -27,4 +27,4 @@ for w in c4 c1 c2 c3; do
   ncu -i $O/prof_$w.ncu-rep --page source --csv 2>/dev/null | gzip > $O/src_$w.csv.gz
   rm -f $O/prof_$w.ncu-rep
 done
-tail -3 $O/pytest_gpu.log $O/smoke.log
+tail -n 3 $O/pytest_gpu.log; tail -n 3 $O/smoke.log
