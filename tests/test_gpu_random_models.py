@@ -3,6 +3,8 @@ two observables), random launch shapes (few points: streaming kernels / graph re
 points: tile kernels, static and plan-specialised, with and without launch-constant caches)
 against the oracle's compensated NLL at 1e-12.  Data are uniform over the observable ranges
 (the NLL does not need the events to follow the pdf)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -76,7 +78,12 @@ def random_model(seed):
     return "\n".join(lines + params + pdfs) + "\n"
 
 
-@pytest.mark.parametrize("seed", range(16))
+# FFB_RANDOM_SEEDS=lo:hi widens the sweep (tools/final_r02.sh runs 16:120 once per round and
+# keeps the log under profiles/)
+_lo, _, _hi = os.environ.get("FFB_RANDOM_SEEDS", "0:16").partition(":")
+
+
+@pytest.mark.parametrize("seed", range(int(_lo), int(_hi)))
 def test_random_model_parity(seed):
     text = random_model(seed)
     m = fb.Model.from_string(text)

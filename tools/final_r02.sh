@@ -6,6 +6,7 @@ TAG=${TAG:-r02_v12}; O=gpurun_out/$TAG; mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $O/smi.txt
 lscpu > $O/lscpu.txt 2>&1
 timeout 1500 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest rc $?" >> $O/pytest_gpu.log
+FFB_RANDOM_SEEDS=16:120 timeout 1500 python -m pytest tests/test_gpu_random_models.py -m gpu -q > $O/pytest_random_sweep.log 2>&1; echo "pytest rc $?" >> $O/pytest_random_sweep.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc $?" >> $O/smoke.log
 timeout 900 python bench.py > $O/bench_default.json 2> $O/bench_default.err
 timeout 900 python bench.py --impl reference > $O/bench_reference.json 2> $O/bench_reference.err
