@@ -42,7 +42,9 @@ std::unique_ptr<ShardGroup> ShardGroup::create_rank(const Model& m, std::shared_
   long long* d = nullptr;
   cuda_check(cudaMalloc(&d, sizeof(long long) * 2 * (1 + world)), "cudaMalloc");
   const long long mine[2] = {l.offset, l.ds->n};
-  cuda_check(cudaMemcpy(d, mine, sizeof(mine), cudaMemcpyHostToDevice), "cudaMemcpy");
+  // (on the group's stream: a pageable cudaMemcpy on the legacy stream may return before its
+  // DMA lands, and l.stream -- non-blocking -- does not order behind it)
+  cuda_check(cudaMemcpyAsync(d, mine, sizeof(mine), cudaMemcpyHostToDevice, l.stream), "cudaMemcpyAsync");
   nccl_check(api.all_gather(d, d + 2, 2, ncclInt64, l.comm, l.stream), "ncclAllGather(offsets)");
   std::vector<long long> all(2 * world);
   cuda_check(cudaMemcpyAsync(all.data(), d + 2, sizeof(long long) * 2 * world, cudaMemcpyDeviceToHost, l.stream),
@@ -100,8 +102,10 @@ void ShardGroup::finish_setup() {
   for (Local& L : local_) {
     DeviceGuard dg(L.device);
     cuda_check(cudaMalloc(&L.d_offsets, sizeof(long long) * world_), "cudaMalloc(offsets)");
-    cuda_check(cudaMemcpy(L.d_offsets, offsets_.data(), sizeof(long long) * world_, cudaMemcpyHostToDevice),
-               "cudaMemcpy(offsets)");
+    cuda_check(cudaMemcpyAsync(L.d_offsets, offsets_.data(), sizeof(long long) * world_, cudaMemcpyHostToDevice,
+                               L.stream),
+               "cudaMemcpyAsync(offsets)");
+    cuda_check(cudaStreamSynchronize(L.stream), "offsets upload");
   }
 }
 
